@@ -1,0 +1,248 @@
+// Operator and restart-loop kernels for sm_100a.
+//
+// K1/K2  stencil_kernel / csr_kernel: y = A·x with every row summed in the
+//        reference's stored (ascending column) order, s = 0.0 start, no FMA
+//        contraction (spmv, csr_matrix.hpp:69-79) — bit-identical to the CPU
+//        reference.  The stencils reproduce gen_laplace2d(nx,ny,5) and
+//        gen_laplace3d (matgen.hpp:134-187) matrix-free: 16 B/row of HBM
+//        traffic instead of CSR's ~76 B/row.
+// K9     the same kernels in residual mode: r = b − A·x fused with the Σr²
+//        partials of ‖r‖ (gmres.hpp:189-194 + dense_matrix.hpp:139).
+// K8     xupdate_kernel: x_new = x + Σ_l y_l q_l, l ascending (gmres.hpp:257-259).
+// K10    scale_div_kernel: v1 = r / γ (gmres.hpp:286-287).
+// All partial sums use one fixed grid and fixed-order trees: results are
+// reproducible run to run (no float atomics).
+#include <cuda_runtime.h>
+
+#include <mutex>
+
+#include "kb_common.hpp"
+#include "kb_kernels.hpp"
+
+namespace kb {
+
+namespace {
+
+constexpr int kBlock = 256;
+
+int num_sms() {
+    static int n = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    });
+    return n;
+}
+
+// Fixed-order block sum; result valid in thread 0.
+__device__ __forceinline__ double block_sum(double v) {
+    __shared__ double warp_part[kBlock / 32];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (lane == 0) warp_part[warp] = v;
+    __syncthreads();
+    double s = 0.0;
+    if (threadIdx.x == 0)
+        for (int w = 0; w < kBlock / 32; ++w) s += warp_part[w];
+    return s;
+}
+
+__device__ __forceinline__ double acc_term(double s, double coeff, double x) {
+    return __dadd_rn(s, __dmul_rn(coeff, x));
+}
+
+template <int DIMS, bool RESID>
+__global__ void __launch_bounds__(kBlock) stencil_kernel(const StencilGeom g, const double* __restrict__ x,
+                                                         const double* __restrict__ halo_lo,
+                                                         const double* __restrict__ halo_hi,
+                                                         const double* __restrict__ b,
+                                                         double* __restrict__ y,
+                                                         double* __restrict__ partials) {
+    // 2-D launch: x over the grid line (ix), y over this rank's grid lines
+    // (grid-stride) — no per-row integer division.  Ranks own whole lines
+    // (2D) / planes (3D); out-of-rank neighbours come from the halo planes.
+    const i64 ix = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    const i64 plane = g.nx * g.ny;
+    const i64 lines = g.nloc / g.nx;
+    const i64 line0 = g.row_begin / g.nx;
+    const i64 z0 = g.row_begin / plane, nzl = g.nloc / plane;
+    double sq = 0.0;
+    for (i64 L = blockIdx.y; L < lines; L += gridDim.y) {
+        if (ix >= g.nx) continue;
+        const i64 i = L * g.nx + ix;  // local row
+        const i64 gl = line0 + L;     // global grid line
+        double s = 0.0;
+        if (DIMS == 2) {
+            if (gl > 0) s = acc_term(s, -1.0, L > 0 ? x[i - g.nx] : halo_lo[ix]);
+            if (ix > 0) s = acc_term(s, -1.0, x[i - 1]);
+            s = acc_term(s, 4.0, x[i]);
+            if (ix + 1 < g.nx) s = acc_term(s, -1.0, x[i + 1]);
+            if (gl + 1 < g.ny) s = acc_term(s, -1.0, L + 1 < lines ? x[i + g.nx] : halo_hi[ix]);
+        } else {
+            const i64 iz = gl / g.ny, iy = gl - iz * g.ny, zl = iz - z0;
+            const i64 hp = iy * g.nx + ix;  // offset inside a halo plane
+            if (iz > 0) s = acc_term(s, -1.0, zl > 0 ? x[i - plane] : halo_lo[hp]);
+            if (iy > 0) s = acc_term(s, -1.0, x[i - g.nx]);
+            if (ix > 0) s = acc_term(s, -1.0, x[i - 1]);
+            s = acc_term(s, 6.0, x[i]);
+            if (ix + 1 < g.nx) s = acc_term(s, -1.0, x[i + 1]);
+            if (iy + 1 < g.ny) s = acc_term(s, -1.0, x[i + g.nx]);
+            if (iz + 1 < g.nz) s = acc_term(s, -1.0, zl + 1 < nzl ? x[i + plane] : halo_hi[hp]);
+        }
+        if (RESID) {
+            const double r = __dsub_rn(b[i], s);
+            y[i] = r;
+            sq = fma(r, r, sq);
+        } else {
+            y[i] = s;
+        }
+    }
+    if (RESID) {
+        const double t = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+template <bool RESID>
+__global__ void __launch_bounds__(kBlock) csr_kernel(i64 nloc, const int64_t* __restrict__ row_ptr,
+                                                     const int32_t* __restrict__ col,
+                                                     const double* __restrict__ vals,
+                                                     const double* __restrict__ x,
+                                                     const double* __restrict__ b, double* __restrict__ y,
+                                                     double* __restrict__ partials) {
+    double sq = 0.0;
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nloc; i += (i64)gridDim.x * blockDim.x) {
+        double s = 0.0;
+        const i64 e = row_ptr[i + 1];
+        for (i64 k = row_ptr[i]; k < e; ++k) s = acc_term(s, __ldg(vals + k), __ldg(x + __ldg(col + k)));
+        if (RESID) {
+            const double r = __dsub_rn(b[i], s);
+            y[i] = r;
+            sq = fma(r, r, sq);
+        } else {
+            y[i] = s;
+        }
+    }
+    if (RESID) {
+        const double t = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.x] = t;
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) dot_kernel(i64 n, const double* __restrict__ a,
+                                                     const double* __restrict__ b,
+                                                     double* __restrict__ partials) {
+    double s = 0.0;
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        s = fma(a[i], b[i], s);
+    const double t = block_sum(s);
+    if (threadIdx.x == 0) partials[blockIdx.x] = t;
+}
+
+__global__ void __launch_bounds__(kBlock) finalize_kernel(const double* __restrict__ partials, int count,
+                                                          double* __restrict__ out) {
+    double s = 0.0;
+    for (int i = threadIdx.x; i < count; i += blockDim.x) s += partials[i];
+    const double t = block_sum(s);
+    if (threadIdx.x == 0) out[0] = t;
+}
+
+__global__ void __launch_bounds__(kBlock) scale_div_kernel(i64 n, const double* __restrict__ r, double gamma,
+                                                           double* __restrict__ out) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        out[i] = r[i] / gamma;
+}
+
+__global__ void __launch_bounds__(kBlock) xupdate_kernel(i64 n, const double* __restrict__ x,
+                                                         const double* __restrict__ q, i64 ldq, int k,
+                                                         const Coef64 y, double* __restrict__ xnew) {
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
+        double s = x[i];
+        for (int l = 0; l < k; ++l) s = fma(y.v[l], q[i + l * ldq], s);
+        xnew[i] = s;
+    }
+}
+
+int grid_for(i64 n) {
+    const i64 g = ceil_div(n, kBlock);
+    return static_cast<int>(std::max<i64>(1, std::min<i64>(g, i64(1) << 30)));  // one row per thread
+}
+
+}  // namespace
+
+int reduce_grid() { return num_sms() * 16; }
+
+dim3 stencil_grid(const StencilGeom& g) {
+    const i64 lines = std::max<i64>(1, g.nloc / g.nx);
+    return dim3(static_cast<unsigned>(ceil_div(g.nx, kBlock)), static_cast<unsigned>(std::min<i64>(lines, 65535)));
+}
+
+int stencil_partials(const StencilGeom& g) {
+    const dim3 d = stencil_grid(g);
+    return static_cast<int>(d.x * d.y);
+}
+
+int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const double* halo_lo,
+                   const double* halo_hi, const double* b, double* y, double* partials, int64_t& launches) {
+    const dim3 grid = stencil_grid(g);
+    if (g.dims == 2) {
+        if (b)
+            stencil_kernel<2, true><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+        else
+            stencil_kernel<2, false><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+    } else {
+        if (b)
+            stencil_kernel<3, true><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+        else
+            stencil_kernel<3, false><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+    }
+    KB_LAUNCHED();
+    ++launches;
+    return b ? static_cast<int>(grid.x * grid.y) : 0;
+}
+
+int launch_csr(cudaStream_t s, i64 nloc, const int64_t* row_ptr, const int32_t* col, const double* vals,
+               const double* x, const double* b, double* y, double* partials, int64_t& launches) {
+    const int grid = b ? reduce_grid() : grid_for(nloc);
+    if (b)
+        csr_kernel<true><<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials);
+    else
+        csr_kernel<false><<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials);
+    KB_LAUNCHED();
+    ++launches;
+    return b ? grid : 0;
+}
+
+void launch_dot(cudaStream_t s, i64 n, const double* a, const double* b, double* partials,
+                int64_t& launches) {
+    dot_kernel<<<reduce_grid(), kBlock, 0, s>>>(n, a, b, partials);
+    KB_LAUNCHED();
+    ++launches;
+}
+
+void launch_finalize_sum(cudaStream_t s, const double* partials, int count, double* out,
+                         int64_t& launches) {
+    finalize_kernel<<<1, kBlock, 0, s>>>(partials, count, out);
+    KB_LAUNCHED();
+    ++launches;
+}
+
+void launch_scale_div(cudaStream_t s, i64 n, const double* r, double gamma, double* out,
+                      int64_t& launches) {
+    scale_div_kernel<<<grid_for(n), kBlock, 0, s>>>(n, r, gamma, out);
+    KB_LAUNCHED();
+    ++launches;
+}
+
+void launch_xupdate(cudaStream_t s, i64 n, const double* x, const double* Q, i64 ldq, int k,
+                    const Coef64& y, double* xnew, int64_t& launches) {
+    xupdate_kernel<<<grid_for(n), kBlock, 0, s>>>(n, x, Q, ldq, k, y, xnew);
+    KB_LAUNCHED();
+    ++launches;
+}
+
+}  // namespace kb

@@ -1,0 +1,491 @@
+// Tall-skinny BlkOrtho kernels for sm_100a (K3 fused Gram, K5 fused update).
+//
+// Both stream a row tile of [V | P] (V = the block being orthogonalized,
+// w ≤ 64 columns; P = a group of prefix basis columns) from HBM into shared
+// memory with one 2-D TMA load per operand per tile (cp.async.bulk.tensor,
+// mbarrier complete_tx), through an S-stage ring driven by one producer warp,
+// and consume it with four compute warps.  Every byte of [V | P] is read from
+// HBM once per launch.
+//
+//  * gram_kernel<NBW>: G = [V | P]ᵀ·V on the DMMA pipe (mma.m8n8k4 f64).
+//    The Gram is the reduction over rows, so rows are the MMA k dimension and
+//    an 8×8 output tile is spread over the 32 lanes (2 doubles per lane): the
+//    whole (c0+w)×w output (≤ 36 tiles, upper triangle only for VᵀV, which
+//    is what gram() computes, dense_kernels.hpp:95-105) stays in registers
+//    for the whole launch.  A fragment for column block b is the same for
+//    the A and the B operand, so one conflict-free LDS per block per four
+//    rows feeds every tile of that block.  Per-CTA partials are reduced by
+//    gram_reduce_kernel in a fixed order (deterministic, no float atomics).
+//  * update_kernel<WMAX>: Q = (V − P·R_col)·R_jj⁻¹ row-locally (direct coalesced
+//    streaming, see below), the order of
+//    bcgs_pip_partial's update + tri_solve_right (block_ortho.hpp:171-176,
+//    dense_kernels.hpp:139-154): vhat_j = V_j − Σ_l R_col(l,j)·p_l (l
+//    ascending), x_j = vhat_j − Σ_{l<j} R(l,j)·x_l, x_j *= 1/R(j,j).  One
+//    thread per row, coefficients broadcast from shared memory, output
+//    written coalesced (may alias V: in place over the basis store).
+#include <cuda.h>
+#include <cuda_runtime.h>
+#include <cudaTypedefs.h>
+
+#include <algorithm>
+#include <cstring>
+#include <mutex>
+#include <vector>
+
+#include "kb_common.hpp"
+#include "kb_kernels.hpp"
+
+namespace kb {
+
+namespace {
+
+constexpr int kConsumerWarps = 4;
+constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + producer warp
+constexpr int kSmemBudget = 200 * 1024;
+
+__device__ __forceinline__ unsigned smem_u32(const void* p) {
+    return static_cast<unsigned>(__cvta_generic_to_shared(p));
+}
+__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
+    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
+    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
+                 "r"(bytes)
+                 : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
+    asm volatile(
+        "{\n\t.reg .pred p;\n"
+        "KB_WAIT_%=:\n\t"
+        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+        "@!p bra KB_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
+        "r"(parity)
+        : "memory");
+}
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
+                                            uint64_t* bar) {
+    asm volatile(
+        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
+        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
+        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
+        : "memory");
+}
+__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
+    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
+                 : "+d"(d0), "+d"(d1)
+                 : "d"(a), "d"(b));
+}
+
+struct TsParams {
+    i64 n;          // rows
+    i64 ntiles;     // ceil(n / tr)
+    int tr;         // rows per tile
+    int w;          // V columns
+    int wslots;     // round_up(w, 8)
+    int cp;         // P columns in this pass
+    int cpslots;    // round_up(cp, 8)
+    int stages;
+    int vv;         // gram: compute the VᵀV tiles in this pass
+    int first;      // update: V holds the raw block (else the running partial)
+    int last;       // update: apply the triangular solve and the scaling
+    unsigned tx_bytes;
+};
+
+// Shared ring set-up common to both kernels.  Returns the stage base.
+__device__ __forceinline__ double* ring_setup(unsigned char* smem, const TsParams& p,
+                                              uint64_t*& full, uint64_t*& empty) {
+    const int slots = p.wslots + p.cpslots;
+    const size_t stage_doubles = static_cast<size_t>(slots) * p.tr;
+    double* ring = reinterpret_cast<double*>(smem);
+    full = reinterpret_cast<uint64_t*>(smem + stage_doubles * 8 * p.stages);
+    empty = full + p.stages;
+    if (threadIdx.x == 0) {
+        for (int s = 0; s < p.stages; ++s) {
+            mbar_init(&full[s], 1);
+            mbar_init(&empty[s], kConsumerWarps);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    // Zero the padding slots (never written by TMA) of every stage.
+    const int padv = p.wslots - p.w, padp = p.cpslots - p.cp;
+    if (padv + padp > 0) {
+        for (int s = 0; s < p.stages; ++s) {
+            double* st = ring + s * stage_doubles;
+            for (int idx = threadIdx.x; idx < (padv + padp) * p.tr; idx += blockDim.x) {
+                const int slot_i = idx / p.tr, r = idx % p.tr;
+                const int slot = slot_i < padv ? p.w + slot_i : p.wslots + p.cp + (slot_i - padv);
+                st[static_cast<size_t>(slot) * p.tr + r] = 0.0;
+            }
+        }
+    }
+    __syncthreads();
+    return ring;
+}
+
+// Producer loop (one elected lane of the last warp).
+__device__ __forceinline__ void ring_produce(const CUtensorMap* map_v, const CUtensorMap* map_p,
+                                            const TsParams& p, double* ring, uint64_t* full,
+                                            uint64_t* empty) {
+    const size_t stage_doubles = static_cast<size_t>(p.wslots + p.cpslots) * p.tr;
+    int it = 0;
+    for (i64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % p.stages;
+        if (it >= p.stages) mbar_wait(&empty[s], ((it / p.stages) - 1) & 1);
+        double* st = ring + s * stage_doubles;
+        mbar_expect_tx(&full[s], p.tx_bytes);
+        const int row0 = static_cast<int>(tile * p.tr);
+        tma_load_2d(st, map_v, row0, 0, &full[s]);
+        if (p.cp > 0) tma_load_2d(st + static_cast<size_t>(p.wslots) * p.tr, map_p, row0, 0, &full[s]);
+    }
+}
+
+// ---------------------------------------------------------------------------
+// K3: fused Gram  G = [V | P]ᵀ V  on DMMA.
+//   Column blocks (8 columns each): b < NBW are V blocks, NBW ≤ b < NBW+nbp
+//   are P blocks.  Tile (ib, jb), jb < NBW, is computed when ib is a P block,
+//   or a V block with ib ≤ jb (upper triangle of VᵀV) and vv is set.
+// ---------------------------------------------------------------------------
+template <int NBW>
+__global__ void __launch_bounds__(kThreads, 1)
+    gram_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_p,
+                const TsParams p, double* __restrict__ partials) {
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t *full, *empty;
+    double* ring = ring_setup(smem, p, full, empty);
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nbp = p.cpslots / 8;
+    const size_t stage_doubles = static_cast<size_t>(p.wslots + p.cpslots) * p.tr;
+
+    if (warp == kConsumerWarps) {
+        if (lane == 0) ring_produce(&map_v, &map_p, p, ring, full, empty);
+        return;
+    }
+
+    double acc[NBW][8][2];
+#pragma unroll
+    for (int jb = 0; jb < NBW; ++jb)
+#pragma unroll
+        for (int ib = 0; ib < 8; ++ib) acc[jb][ib][0] = acc[jb][ib][1] = 0.0;
+
+    const int frag_off = (lane >> 2) * p.tr + (lane & 3);
+    const int nchunks = p.tr / 4;
+    int it = 0;
+    for (i64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
+        const int s = it % p.stages;
+        mbar_wait(&full[s], (it / p.stages) & 1);
+        const double* st = ring + s * stage_doubles;
+        for (int c = (warp + it) & 3; c < nchunks; c += kConsumerWarps) {
+            const double* base = st + frag_off + 4 * c;
+            double f[8];
+#pragma unroll
+            for (int b = 0; b < 8; ++b)
+                f[b] = (b < NBW + nbp) ? base[static_cast<size_t>(8 * b) * p.tr] : 0.0;
+#pragma unroll
+            for (int jb = 0; jb < NBW; ++jb) {
+#pragma unroll
+                for (int ib = 0; ib < 8; ++ib) {
+                    if (ib < NBW) {
+                        if (ib <= jb && p.vv) dmma(acc[jb][ib][0], acc[jb][ib][1], f[ib], f[jb]);
+                    } else if (ib - NBW < nbp) {
+                        dmma(acc[jb][ib][0], acc[jb][ib][1], f[ib], f[jb]);
+                    }
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+    }
+
+    // Cross-warp reduction in fixed warp order, through the (now idle) ring.
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+    double* scratch = ring;  // [warp][NBW*8][64]
+    const int e0 = (lane >> 2) + 8 * (2 * (lane & 3));
+#pragma unroll
+    for (int jb = 0; jb < NBW; ++jb)
+#pragma unroll
+        for (int ib = 0; ib < 8; ++ib) {
+            double* t = scratch + (static_cast<size_t>(warp) * NBW * 8 + jb * 8 + ib) * 64;
+            t[e0] = acc[jb][ib][0];
+            t[e0 + 8] = acc[jb][ib][1];
+        }
+    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
+    const int per_warp = NBW * 8 * 64;
+    double* out = partials + static_cast<size_t>(blockIdx.x) * per_warp;
+    for (int e = threadIdx.x; e < per_warp; e += kConsumerWarps * 32) {
+        double sum = scratch[e];
+#pragma unroll
+        for (int w = 1; w < kConsumerWarps; ++w) sum += scratch[static_cast<size_t>(w) * per_warp + e];
+        out[e] = sum;
+    }
+}
+
+struct TileList {
+    int count;
+    int id[64];  // jb * 8 + ib
+};
+
+// One warp per output entry: lanes sum the per-CTA partials with a fixed
+// stride, then a fixed xor tree.  Deterministic for a given grid size.
+__global__ void gram_reduce_kernel(const double* __restrict__ partials, int grid, int per_cta,
+                                   const TileList tiles, double* __restrict__ packed) {
+    const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
+    const int lane = threadIdx.x & 31;
+    if (gw >= tiles.count * 64) return;
+    const int t = gw >> 6, e = gw & 63;
+    const size_t off = static_cast<size_t>(tiles.id[t]) * 64 + e;
+    double s = 0.0;
+    for (int c = lane; c < grid; c += 32) s += partials[static_cast<size_t>(c) * per_cta + off];
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
+    if (lane == 0) packed[gw] = s;
+}
+
+// ---------------------------------------------------------------------------
+// K5: fused update  out = (V − P·R_col)·R_jj⁻¹, one thread per row, in place
+// over the store (out may alias V; P never aliases out).  Coalesced 256-byte
+// warp loads/stores straight from HBM at high occupancy; the coefficients are
+// broadcast from shared memory.  Both loops are right-looking so every row
+// keeps w independent FMA chains, while each element still receives its
+// terms in the reference's order (l ascending, then ×1/R(j,j)).
+// coef layout (doubles): nrc[cp][WMAX] = −R_col, nrjj[WMAX][WMAX] = −R_jj(l,j)
+// for l < j, inv[WMAX] = 1/R_jj(j,j).
+// ---------------------------------------------------------------------------
+template <int WMAX>
+__global__ void __launch_bounds__(256)
+    update_kernel(i64 n, const double* __restrict__ P, i64 ldp, int cp, const double* V, i64 ldv, int w,
+                  const double* __restrict__ coef, int triangular, double* out, i64 ldo) {
+    extern __shared__ __align__(16) double c_sm[];
+    const int ncoef = (cp + WMAX + 1) * WMAX;
+    for (int i = threadIdx.x; i < ncoef; i += blockDim.x) c_sm[i] = coef[i];
+    __syncthreads();
+    const double* nrc = c_sm;
+    const double* nrjj = c_sm + static_cast<size_t>(cp) * WMAX;
+    const double* inv = nrjj + WMAX * WMAX;
+    for (i64 row = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; row < n;
+         row += static_cast<i64>(gridDim.x) * blockDim.x) {
+        double acc[WMAX];
+#pragma unroll
+        for (int j = 0; j < WMAX; ++j) acc[j] = (j < w) ? V[row + j * ldv] : 0.0;
+        const double* prow = P + row;
+        int l = 0;
+        for (; l + 4 <= cp; l += 4) {
+            double pv[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pv[u] = __ldg(prow + (l + u) * ldp);
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double* cr = nrc + (l + u) * WMAX;
+#pragma unroll
+                for (int j = 0; j < WMAX; ++j)
+                    if (j < w) acc[j] = fma(cr[j], pv[u], acc[j]);
+            }
+        }
+        for (; l < cp; ++l) {
+            const double pv = __ldg(prow + l * ldp);
+            const double* cr = nrc + l * WMAX;
+#pragma unroll
+            for (int j = 0; j < WMAX; ++j)
+                if (j < w) acc[j] = fma(cr[j], pv, acc[j]);
+        }
+        if (triangular) {
+#pragma unroll
+            for (int k = 0; k < WMAX; ++k) {
+                if (k < w) {
+                    acc[k] *= inv[k];
+#pragma unroll
+                    for (int j = k + 1; j < WMAX; ++j)
+                        if (j < w) acc[j] = fma(nrjj[k * WMAX + j], acc[k], acc[j]);
+                }
+            }
+        }
+#pragma unroll
+        for (int j = 0; j < WMAX; ++j)
+            if (j < w) out[row + j * ldo] = acc[j];
+    }
+}
+
+
+// ---------------------------------------------------------------------------
+// Host side: tensor maps, geometry, launches.
+// ---------------------------------------------------------------------------
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+    static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        cudaDriverEntryPointQueryResult q;
+        void* p = nullptr;
+        if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+            q == cudaDriverEntryPointSuccess)
+            fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+    });
+    if (!fn) fail(KRY_CUDA_ERROR, "cuTensorMapEncodeTiled unavailable");
+    return fn;
+}
+
+CUtensorMap make_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows) {
+    CUtensorMap m;
+    std::memset(&m, 0, sizeof(m));
+    if (cols <= 0 || base == nullptr) return m;  // unused operand
+    if ((reinterpret_cast<uintptr_t>(base) & 15) != 0 || (ld & 1) != 0)
+        fail(KRY_INTERNAL, "TMA operand must be 16-byte aligned with an even leading dimension");
+    cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols)};
+    cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(cols)};
+    cuuint32_t estr[2] = {1, 1};
+    CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
+                             strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
+                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    if (r != CUDA_SUCCESS) fail(KRY_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
+    return m;
+}
+
+int sm_count() {
+    static int n = 0;
+    static std::once_flag once;
+    std::call_once(once, [] {
+        int dev = 0;
+        cudaGetDevice(&dev);
+        cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, dev);
+        if (n <= 0) n = 148;
+    });
+    return n;
+}
+
+template <typename K>
+void set_smem(K kernel, size_t bytes) {
+    KB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                 static_cast<int>(bytes)));
+}
+
+TsParams geometry(i64 n, int w, int cp, bool gram) {
+    TsParams p{};
+    p.n = n;
+    p.w = w;
+    p.wslots = static_cast<int>(round_up(w, 8));
+    p.cp = cp;
+    p.cpslots = static_cast<int>(round_up(cp, 8));
+    const int slots = p.wslots + p.cpslots;
+    if (gram) {
+        // rows ≡ 4 (mod 16): the DMMA fragment loads are bank-conflict free.
+        static const int cand[] = {244, 196, 132, 68};
+        p.tr = 68;
+        for (int c : cand)
+            if (static_cast<size_t>(c) * slots * 8 <= 36 * 1024) {
+                p.tr = c;
+                break;
+            }
+    } else {
+        p.tr = 128;  // one row per consumer thread
+    }
+    const size_t stage_bytes = static_cast<size_t>(slots) * p.tr * 8;
+    const int wm = w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64;
+    const size_t coef_bytes = gram ? 0 : static_cast<size_t>(cp + wm + 1) * wm * 8 + 1024;
+    int st = static_cast<int>((kSmemBudget - coef_bytes) / stage_bytes);
+    p.stages = std::max(2, std::min(8, st));
+    p.ntiles = ceil_div(n, p.tr);
+    p.tx_bytes = static_cast<unsigned>(static_cast<size_t>(w + cp) * p.tr * 8);
+    return p;
+}
+
+size_t ring_bytes(const TsParams& p) {
+    return static_cast<size_t>(p.wslots + p.cpslots) * p.tr * 8 * p.stages + 16 * p.stages + 64;
+}
+
+}  // namespace
+
+// Column groups of the prefix so that round_up(w,8) + round_up(group,8) ≤ 64.
+std::vector<std::pair<i64, i64>> prefix_groups(i64 c0, i64 w) {
+    std::vector<std::pair<i64, i64>> g;
+    const i64 wslots = round_up(w, 8);
+    if (wslots > 64) fail(KRY_UNSUPPORTED, "block width above 64 columns is not supported on the device path");
+    const i64 room = 64 - wslots;
+    if (c0 > 0 && room == 0) fail(KRY_UNSUPPORTED, "block width 57..64 with a non-empty prefix is not supported");
+    for (i64 b = 0; b < c0; b += room) g.emplace_back(b, std::min(room, c0 - b));
+    return g;
+}
+
+i64 gram_scratch_doubles(i64 w) {
+    return static_cast<i64>(sm_count()) * round_up(w, 8) / 8 * 8 * 64;
+}
+
+void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V,
+                      i64 ldv, i64 w, bool vv, double* d_partials, double* d_packed,
+                      std::vector<int>& tile_ids, int64_t& launches) {
+    TsParams p = geometry(n, static_cast<int>(w), static_cast<int>(cp), true);
+    p.vv = vv ? 1 : 0;
+    const int nbw = p.wslots / 8, nbp = p.cpslots / 8;
+    tile_ids.clear();
+    for (int jb = 0; jb < nbw; ++jb)
+        for (int ib = 0; ib < 8; ++ib) {
+            const bool ok = (ib < nbw) ? (ib <= jb && vv) : (ib - nbw < nbp);
+            if (ok) tile_ids.push_back(jb * 8 + ib);
+        }
+    if (tile_ids.empty()) return;
+    CUtensorMap mv = make_map(V, ldv, n, w, p.tr);
+    CUtensorMap mp = make_map(P, ldp, n, cp, p.tr);
+    const int grid = static_cast<int>(std::min<i64>(sm_count(), std::max<i64>(1, p.ntiles)));
+    const size_t red_bytes = static_cast<size_t>(kConsumerWarps) * nbw * 8 * 64 * 8;
+    const size_t smem = std::max(ring_bytes(p), red_bytes) + 1024;
+    switch (nbw) {
+#define KB_GRAM_CASE(NB)                                                                   \
+    case NB:                                                                               \
+        set_smem(gram_kernel<NB>, smem);                                                   \
+        gram_kernel<NB><<<grid, kThreads, smem, stream>>>(mv, mp, p, d_partials);          \
+        break;
+        KB_GRAM_CASE(1)
+        KB_GRAM_CASE(2)
+        KB_GRAM_CASE(3)
+        KB_GRAM_CASE(4)
+        KB_GRAM_CASE(5)
+        KB_GRAM_CASE(6)
+        KB_GRAM_CASE(7)
+        KB_GRAM_CASE(8)
+#undef KB_GRAM_CASE
+        default:
+            fail(KRY_UNSUPPORTED, "gram width");
+    }
+    KB_LAUNCHED();
+    TileList tl{};
+    tl.count = static_cast<int>(tile_ids.size());
+    for (int i = 0; i < tl.count; ++i) tl.id[i] = tile_ids[i];
+    const int warps = tl.count * 64;
+    gram_reduce_kernel<<<ceil_div(warps * 32, 256), 256, 0, stream>>>(d_partials, grid, nbw * 8 * 64,
+                                                                       tl, d_packed);
+    KB_LAUNCHED();
+    launches += 2;
+}
+
+int update_wmax(i64 w) { return w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64; }
+
+void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
+                   i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches) {
+    const int wmax = update_wmax(w);
+    const size_t smem = static_cast<size_t>(cp + wmax + 1) * wmax * 8;
+    if (smem > 200 * 1024) fail(KRY_UNSUPPORTED, "update coefficients exceed shared memory");
+    auto go = [&](auto kernel) {
+        set_smem(kernel, smem);
+        int per_sm = 0;
+        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem));
+        const i64 want = ceil_div(n, 256);
+        const int grid = static_cast<int>(std::max<i64>(1, std::min<i64>(want, static_cast<i64>(sm_count()) * std::max(per_sm, 1))));
+        kernel<<<grid, 256, smem, stream>>>(n, P, ldp, static_cast<int>(cp), V, ldv, static_cast<int>(w), d_coef,
+                                            triangular ? 1 : 0, out, ldo);
+    };
+    switch (wmax) {
+        case 8: go(update_kernel<8>); break;
+        case 16: go(update_kernel<16>); break;
+        case 32: go(update_kernel<32>); break;
+        default: go(update_kernel<64>); break;
+    }
+    KB_LAUNCHED();
+    launches += 1;
+}
+
+
+}  // namespace kb

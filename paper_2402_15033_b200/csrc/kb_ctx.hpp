@@ -1,0 +1,111 @@
+// Execution context: one device, one non-blocking stream, an optional NCCL
+// communicator (one process per GPU; rows partitioned across ranks), the
+// scratch buffers of the hot path and the CUDA-event phase timers.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <nccl.h>
+
+#include <array>
+#include <vector>
+
+#include "kb_common.hpp"
+
+namespace kb {
+
+// RAII device allocation.
+struct DevBuf {
+    double* p = nullptr;
+    size_t bytes = 0;
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+    DevBuf(DevBuf&& o) noexcept : p(o.p), bytes(o.bytes) { o.p = nullptr; o.bytes = 0; }
+    DevBuf& operator=(DevBuf&& o) noexcept {
+        if (this != &o) { release(); p = o.p; bytes = o.bytes; o.p = nullptr; o.bytes = 0; }
+        return *this;
+    }
+    ~DevBuf() { release(); }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        bytes = 0;
+    }
+    // Grow to at least `b` bytes (contents not preserved).
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        release();
+        void* q = nullptr;
+        KB_CUDA(cudaMalloc(&q, b));
+        p = static_cast<double*>(q);
+        bytes = b;
+    }
+    template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
+};
+
+// RAII pinned host allocation.
+struct HostBuf {
+    double* p = nullptr;
+    size_t bytes = 0;
+    HostBuf() = default;
+    HostBuf(const HostBuf&) = delete;
+    HostBuf& operator=(const HostBuf&) = delete;
+    ~HostBuf() { if (p) cudaFreeHost(p); }
+    void ensure(size_t b) {
+        if (b <= bytes) return;
+        if (p) cudaFreeHost(p);
+        p = nullptr;
+        bytes = 0;
+        void* q = nullptr;
+        KB_CUDA(cudaMallocHost(&q, b));
+        p = static_cast<double*>(q);
+        bytes = b;
+    }
+};
+
+enum Phase { PH_MPK = 0, PH_ORTHO, PH_GRAM, PH_UPDATE, PH_RESTART, PH_COUNT };
+
+struct Ctx {
+    int device = 0;
+    int nranks = 1;
+    int rank = 0;
+    cudaStream_t stream = nullptr;
+    ncclComm_t comm = nullptr;
+    bool timing = false;
+    int64_t launches = 0;
+    int64_t allreduces = 0;
+    double gram_bytes = 0.0, update_bytes = 0.0;  // algorithmic, this rank
+    int64_t gram_launches = 0, update_launches = 0;
+
+    // scratch
+    DevBuf partials;      // reduce_grid() doubles + scalars
+    DevBuf gram_partials; // per-CTA Gram partials
+    DevBuf gram_packed;   // packed Gram tiles (all prefix groups)
+    DevBuf coef;          // update coefficients (all passes)
+    HostBuf h_packed, h_coef, h_scalar;
+
+    // phase timers
+    std::array<double, PH_COUNT> seconds{};
+    std::vector<cudaEvent_t> pool;
+    struct Pending { int phase; cudaEvent_t a, b; };
+    std::vector<Pending> pending;
+
+    Ctx(int dev, int nr, int rk, const void* nccl_id);
+    ~Ctx();
+
+    void sync();
+    // Timer: begin() returns a token; end(token) closes it.
+    cudaEvent_t begin_phase();
+    void end_phase(int phase, cudaEvent_t start);
+    void resolve_timers();  // after a stream sync: accumulate elapsed times
+
+    // Σ over ranks, in place on the device (no-op for one rank).
+    void allreduce_sum(double* d, size_t count);
+    // Device scalar sum of r² style partials → host value (allreduced).
+    double finalize_scalar(const double* d_partials, int count);
+};
+
+// Host thread-local: device of the current call.
+void bind_device(Ctx& c);
+
+}  // namespace kb

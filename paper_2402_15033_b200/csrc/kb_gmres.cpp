@@ -1,0 +1,262 @@
+#include "kb_gmres.hpp"
+
+#include <chrono>
+#include <cmath>
+#include <limits>
+#include <utility>
+
+namespace kb {
+
+void validate_config(const kry_solver_config& c) {
+    // SolverConfig::validate (gmres.hpp:28-35)
+    if (c.restart_len <= 0 || c.step <= 0 || c.restart_len % c.step != 0)
+        fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: step size must divide the restart length");
+    const i64 shat = c.big_step == 0 ? c.restart_len : c.big_step;
+    if (shat < c.step || shat > c.restart_len || shat % c.step != 0)
+        fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: second step size must be a multiple of s in [s, m]");
+    if (!(c.rel_tol > 0.0)) fail(KRY_INVALID_ARGUMENT, "rel_tol must be positive");
+}
+
+namespace {
+
+struct Vec {
+    DevBuf buf;
+    double* p() const { return buf.p; }
+};
+
+}  // namespace
+
+Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, const kry_solver_config& cfg_in,
+             bool standard_mode, double* d_x_out) {
+    kry_solver_config cfg = cfg_in;
+    if (standard_mode) {  // standard_gmres (gmres.hpp:404-411)
+        cfg.step = 1;
+        cfg.big_step = 0;
+        cfg.scheme_kind = KRY_ORTHO_BCGS2_CHOLQR2;
+        cfg.scheme_big_panel_size = 0;
+    }
+    validate_config(cfg);
+    const auto t_start = std::chrono::steady_clock::now();
+    const i64 n = op.nloc;
+    const i64 m = cfg.restart_len;
+    const i64 s = standard_mode ? 1 : cfg.step;
+    const bool two_stage = (cfg.scheme_kind == KRY_ORTHO_TWO_STAGE) && !standard_mode;
+    const i64 shat = two_stage ? (cfg.big_step == 0 ? m : cfg.big_step) : s;
+
+    Report rep;
+    const size_t vbytes = static_cast<size_t>(device_ld(n)) * 8;
+    DevBuf x, xn, r, rn;
+    x.ensure(vbytes);
+    xn.ensure(vbytes);
+    r.ensure(vbytes);
+    rn.ensure(vbytes);
+    if (d_x0)
+        KB_CUDA(cudaMemcpyAsync(x.p, d_x0, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+    else
+        KB_CUDA(cudaMemsetAsync(x.p, 0, vbytes, ctx.stream));
+
+    // r = b − A·x and ‖r‖ in one fused pass (K9).  The norm of the current
+    // r is cached: the reference recomputes norm2(r) on the same vector.
+    auto residual = [&](const double* xv, double* rv) -> double {
+        cudaEvent_t t0 = ctx.begin_phase();
+        const int cnt = op.apply(xv, rv, d_b);
+        const double sq = ctx.finalize_scalar(op.partials.p, cnt);
+        ctx.end_phase(PH_RESTART, t0);
+        return std::sqrt(sq);
+    };
+    double r_norm = residual(x.p, r.p);
+    const double r0 = r_norm;
+    rep.initial_residual = r0;
+    auto finish = [&]() {
+        if (d_x_out)
+            KB_CUDA(cudaMemcpyAsync(d_x_out, x.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+        ctx.sync();
+        ctx.resolve_timers();
+        rep.wall_seconds =
+            std::chrono::duration<double>(std::chrono::steady_clock::now() - t_start).count();
+    };
+    if (r0 == 0.0) {
+        rep.status = KRY_STATUS_CONVERGED;
+        finish();
+        return rep;
+    }
+
+    Store store(ctx, n, m, s, shat);
+    const int scheme = cfg.scheme_kind;
+
+    auto usable_cols = [&]() -> i64 {
+        i64 k = store.filled() == 0 ? 0 : store.filled() - 1;
+        if (store.has_seam_column()) ++k;
+        const Upper& rr = store.coefficients();
+        for (i64 j = 0; j < k; ++j)
+            if (rr(j, j) == 0.0) return j;
+        return k;
+    };
+
+    struct Check {
+        bool implicit_crossed = false;
+        bool applied = false;
+        double explicit_rel = std::numeric_limits<double>::infinity();
+    };
+
+    // gmres.hpp:247-269
+    auto check_and_update = [&](double gamma, bool force) -> Check {
+        Check res;
+        const i64 k = usable_cols();
+        if (k == 0) return res;
+        Mat h = assemble_hessenberg(store.coefficients(), k, store.block_records());
+        Lsq lsq = solve_hessenberg_lsq(h, gamma);
+        res.implicit_crossed = lsq.implicit_residual <= cfg.rel_tol * r0;
+        if (!res.implicit_crossed && !force) return res;
+
+        cudaEvent_t t0 = ctx.begin_phase();
+        const double* src = x.p;
+        if (lsq.valid_cols == 0)
+            KB_CUDA(cudaMemcpyAsync(xn.p, x.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+        for (i64 l0 = 0; l0 < lsq.valid_cols; l0 += 64) {
+            Coef64 y{};
+            const int cnt = static_cast<int>(std::min<i64>(64, lsq.valid_cols - l0));
+            for (int i = 0; i < cnt; ++i) y.v[i] = lsq.y[l0 + i];
+            launch_xupdate(ctx.stream, n, src, store.col(l0), store.ld(), cnt, y, xn.p, ctx.launches);
+            src = xn.p;
+        }
+        rep.mpk_bytes += 0;  // the residual's SpMV is restart-loop traffic
+        ctx.end_phase(PH_RESTART, t0);
+        const double rnv = residual(xn.p, rn.p);
+        res.explicit_rel = rnv / r0;
+        if (rnv <= gamma * (1.0 + 1e-12)) {
+            std::swap(x.p, xn.p);
+            std::swap(r.p, rn.p);
+            r_norm = rnv;
+            res.applied = true;
+        }
+        return res;
+    };
+
+    bool done = false;
+    int stagnation_strikes = 0;
+    const i64 blocks = m / s;
+
+    while (!done) {
+        const double gamma = r_norm;
+        if (gamma / r0 <= cfg.rel_tol) {
+            rep.status = KRY_STATUS_CONVERGED;
+            break;
+        }
+        if (rep.iterations >= cfg.max_iters) {
+            rep.status = KRY_STATUS_MAX_ITERS;
+            break;
+        }
+        store.reset();
+        {
+            cudaEvent_t t0 = ctx.begin_phase();
+            launch_scale_div(ctx.stream, n, r.p, gamma, store.col(0), ctx.launches);  // v1 = r/γ (K10)
+            ctx.end_phase(PH_RESTART, t0);
+        }
+        if (standard_mode) store.seed_unit_column(store.col(0));
+
+        bool updated_this_cycle = false;
+        for (i64 j = 0; j < blocks && !done; ++j) {
+            Outcome oc;
+            if (standard_mode) {
+                const i64 f = store.filled();
+                cudaEvent_t t0 = ctx.begin_phase();
+                op.apply(store.col(f - 1), store.col(f));
+                ctx.end_phase(PH_MPK, t0);
+                rep.mpk_bytes += op.bytes_per_apply();
+                cudaEvent_t t1 = ctx.begin_phase();
+                oc = store.append_block(store.col(f), store.ld(), 1, false, scheme, 0, rep.sync);
+                ctx.end_phase(PH_ORTHO, t1);
+            } else {
+                const i64 c0 = (j == 0) ? 0 : store.filled() - 1;
+                cudaEvent_t t0 = ctx.begin_phase();
+                store.mpk(op, c0, s);
+                ctx.end_phase(PH_MPK, t0);
+                rep.mpk_bytes += s * op.bytes_per_apply();
+                cudaEvent_t t1 = ctx.begin_phase();
+                if (two_stage)
+                    oc = store.preprocess_block(store.col(c0), store.ld(), s + 1, j != 0, rep.sync);
+                else
+                    oc = store.append_block(store.col(c0), store.ld(), s + 1, j != 0, scheme,
+                                            cfg.scheme_big_panel_size, rep.sync);
+                ctx.end_phase(PH_ORTHO, t1);
+            }
+            rep.iterations += s;
+
+            if (oc.breakdown || oc.truncated) {
+                rep.breakdown = true;
+                rep.breakdown_kappa = oc.kappa_estimate;
+                if (two_stage && store.big_panel_open()) {
+                    cudaEvent_t t1 = ctx.begin_phase();
+                    store.finalize_big_panel(rep.sync);
+                    ctx.end_phase(PH_ORTHO, t1);
+                }
+                Check res = check_and_update(gamma, true);
+                updated_this_cycle = true;
+                rep.status = (res.explicit_rel <= cfg.rel_tol) ? KRY_STATUS_CONVERGED : KRY_STATUS_ORTHO_BREAKDOWN;
+                done = true;
+                break;
+            }
+
+            if (two_stage) {
+                const bool last_block = (j + 1 == blocks);
+                if (store.big_panel_full() || last_block) {
+                    cudaEvent_t t1 = ctx.begin_phase();
+                    Outcome fin = store.finalize_big_panel(rep.sync);
+                    ctx.end_phase(PH_ORTHO, t1);
+                    if (fin.breakdown) {
+                        rep.breakdown = true;
+                        rep.breakdown_kappa = fin.kappa_estimate;
+                        Check res = check_and_update(gamma, true);
+                        updated_this_cycle = true;
+                        rep.status =
+                            (res.explicit_rel <= cfg.rel_tol) ? KRY_STATUS_CONVERGED : KRY_STATUS_ORTHO_BREAKDOWN;
+                        done = true;
+                        break;
+                    }
+                } else {
+                    continue;  // convergence is only observable per big panel
+                }
+            }
+
+            Check res = check_and_update(gamma, false);
+            if (res.implicit_crossed) {
+                updated_this_cycle = true;
+                if (res.explicit_rel <= cfg.rel_tol) {
+                    rep.status = KRY_STATUS_CONVERGED;
+                    done = true;
+                } else {
+                    break;  // implicit check was optimistic: restart from the update
+                }
+            }
+        }
+
+        if (!updated_this_cycle) check_and_update(gamma, true);
+        const double rnorm = r_norm;
+        rep.cycle_residuals.push_back(rnorm / r0);
+        ctx.resolve_timers();
+        if (done) break;
+        ++rep.restarts;
+        if (rnorm / r0 <= cfg.rel_tol) {
+            rep.status = KRY_STATUS_CONVERGED;
+            break;
+        }
+        if (rnorm > 0.99 * gamma) {
+            if (++stagnation_strikes >= 2) {
+                rep.status = KRY_STATUS_STAGNATION;
+                break;
+            }
+        } else {
+            stagnation_strikes = 0;
+        }
+    }
+
+    rep.final_relative_residual = r_norm / r0;
+    if (rep.iterations > 0)
+        rep.reduces_per_iteration = static_cast<double>(rep.sync.reduces) / static_cast<double>(rep.iterations);
+    rep.ortho_bytes = store.ortho_bytes;
+    finish();
+    return rep;
+}
+
+}  // namespace kb

@@ -1,0 +1,56 @@
+// Host-callable launchers for the sm_100a kernels of the hot path.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <utility>
+#include <vector>
+
+#include "kb_common.hpp"
+
+namespace kb {
+
+// ---- k_tsqr.cu : BlkOrtho (K3 Gram, K5 update) ---------------------------
+std::vector<std::pair<i64, i64>> prefix_groups(i64 c0, i64 w);
+i64 gram_scratch_doubles(i64 w);
+// Packed G tiles for one prefix group: tile_ids[t] = jb*8 + ib, 64 entries
+// per tile (8×8 column-major), written to d_packed in tile order.
+void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V,
+                      i64 ldv, i64 w, bool vv, double* d_partials, double* d_packed,
+                      std::vector<int>& tile_ids, int64_t& launches);
+int update_wmax(i64 w);
+// out = (V − P·R_col)·R_jj⁻¹ (triangular) or V − P·R_col; out may alias V.
+void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
+                   i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches);
+
+// ---- k_ops.cu : operators (K1/K2), restart-loop vectors (K8-K10) ---------
+struct StencilGeom {
+    int dims;        // 2 or 3
+    i64 nx, ny, nz;  // grid
+    i64 row_begin;   // first global row owned
+    i64 nloc;        // rows owned
+    i64 halo;        // halo length (nx for 2D, nx*ny for 3D)
+};
+// y = A·x (b == nullptr) or r = b − A·x with Σr² partials (b != nullptr);
+// returns the number of partials written.
+int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const double* halo_lo,
+                   const double* halo_hi, const double* b, double* y, double* partials, int64_t& launches);
+int stencil_partials(const StencilGeom& g);
+// CSR rows (row_ptr local, from 0) gathering x through int32 indices.
+int launch_csr(cudaStream_t s, i64 nloc, const int64_t* row_ptr, const int32_t* col, const double* vals,
+               const double* x, const double* b, double* y, double* partials, int64_t& launches);
+int reduce_grid();  // fixed grid of every partial-sum kernel (determinism)
+void launch_dot(cudaStream_t s, i64 n, const double* a, const double* b, double* partials,
+                int64_t& launches);
+void launch_finalize_sum(cudaStream_t s, const double* partials, int count, double* out,
+                         int64_t& launches);
+void launch_scale_div(cudaStream_t s, i64 n, const double* r, double gamma, double* out,
+                      int64_t& launches);
+struct Coef64 {
+    double v[64];
+};
+void launch_xupdate(cudaStream_t s, i64 n, const double* x, const double* Q, i64 ldq, int k,
+                    const Coef64& y, double* xnew, int64_t& launches);
+
+}  // namespace kb

@@ -1,0 +1,154 @@
+#include "kb_operator.hpp"
+
+#include <algorithm>
+#include <limits>
+#include <vector>
+
+namespace kb {
+
+#define KB_NCCL(expr)                                                                      \
+    do {                                                                                   \
+        ncclResult_t kb_r_ = (expr);                                                       \
+        if (kb_r_ != ncclSuccess)                                                          \
+            ::kb::fail(KRY_NCCL_ERROR, std::string(#expr) + ": " + ncclGetErrorString(kb_r_)); \
+    } while (0)
+
+Operator* make_laplace(Ctx& ctx, int dims, i64 nx, i64 ny, i64 nz) {
+    if (dims == 2) {
+        if (nx < 2 || ny < 2) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: gen_laplace2d needs dimensions >= 2");
+    } else {
+        if (nx < 2 || ny < 2 || nz < 2)
+            fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: gen_laplace3d needs dimensions >= 2");
+    }
+    auto* op = new Operator;
+    op->ctx = &ctx;
+    op->kind = dims == 2 ? Operator::LAPLACE2D : Operator::LAPLACE3D;
+    const i64 lines = dims == 2 ? ny : nz;
+    const i64 plane = dims == 2 ? nx : nx * ny;
+    if (lines < ctx.nranks) {
+        delete op;
+        fail(KRY_INVALID_ARGUMENT, "fewer grid lines than ranks");
+    }
+    const i64 l0 = ctx.rank * lines / ctx.nranks, l1 = (ctx.rank + 1) * lines / ctx.nranks;
+    op->n_global = plane * lines;
+    op->row_begin = l0 * plane;
+    op->nloc = (l1 - l0) * plane;
+    op->nnz_local = 0;
+    op->geom = StencilGeom{dims, nx, ny, dims == 2 ? 1 : nz, op->row_begin, op->nloc, plane};
+    if (ctx.nranks > 1) {
+        op->halo_lo.ensure(static_cast<size_t>(plane) * 8);
+        op->halo_hi.ensure(static_cast<size_t>(plane) * 8);
+    }
+    op->partials.ensure(static_cast<size_t>(stencil_partials(op->geom) + 64) * 8);
+    return op;
+}
+
+Operator* make_csr(Ctx& ctx, i64 n_global, i64 row_begin, i64 nloc, const int64_t* rp, const int64_t* ci,
+                   const double* v) {
+    // CsrMatrix::validate (csr_matrix.hpp:25-38), restricted to the local rows.
+    dim_check(nloc >= 0 && row_begin >= 0 && row_begin + nloc <= n_global, "csr row range");
+    dim_check(rp[0] == 0, "row_ptr bounds");
+    for (i64 i = 0; i < nloc; ++i) {
+        dim_check(rp[i] <= rp[i + 1], "row_ptr not monotone");
+        for (i64 k = rp[i]; k < rp[i + 1]; ++k) {
+            dim_check(ci[k] >= 0 && ci[k] < n_global, "column index out of range");
+            dim_check(k == rp[i] || ci[k] > ci[k - 1], "column indices not strictly increasing");
+        }
+    }
+    auto* op = new Operator;
+    op->ctx = &ctx;
+    op->kind = Operator::CSR;
+    op->n_global = n_global;
+    op->row_begin = row_begin;
+    op->nloc = nloc;
+    op->nnz_local = rp[nloc];
+
+    // Rank layout (row_begin, nloc of every rank) for the x gather.
+    std::vector<int64_t> layout(2 * ctx.nranks, 0);
+    layout[2 * ctx.rank] = row_begin;
+    layout[2 * ctx.rank + 1] = nloc;
+    if (ctx.nranks > 1) {
+        DevBuf d;
+        d.ensure(layout.size() * 8);
+        KB_CUDA(cudaMemcpyAsync(d.p, layout.data() + 2 * ctx.rank, 16, cudaMemcpyHostToDevice, ctx.stream));
+        KB_NCCL(ncclAllGather(d.as<int64_t>() + 2 * ctx.rank, d.as<int64_t>(), 2, ncclInt64, ctx.comm,
+                              ctx.stream));
+        KB_CUDA(cudaMemcpyAsync(layout.data(), d.p, layout.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));
+        ctx.sync();
+    }
+    i64 max_rows = 0;
+    for (int r = 0; r < ctx.nranks; ++r) max_rows = std::max<i64>(max_rows, layout[2 * r + 1]);
+    op->max_rows = max_rows;
+    if (static_cast<double>(max_rows) * ctx.nranks >= static_cast<double>(std::numeric_limits<int32_t>::max())) {
+        delete op;
+        fail(KRY_UNSUPPORTED, "CSR gather index exceeds int32");
+    }
+    std::vector<int32_t> col(static_cast<size_t>(op->nnz_local));
+    for (i64 k = 0; k < op->nnz_local; ++k) {
+        const i64 g = ci[k];
+        if (ctx.nranks == 1) {
+            col[k] = static_cast<int32_t>(g);
+            continue;
+        }
+        int owner = -1;
+        for (int r = 0; r < ctx.nranks; ++r)
+            if (g >= layout[2 * r] && g < layout[2 * r] + layout[2 * r + 1]) { owner = r; break; }
+        if (owner < 0) {
+            delete op;
+            fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: column not owned by any rank");
+        }
+        col[k] = static_cast<int32_t>(owner * max_rows + (g - layout[2 * owner]));
+    }
+    op->row_ptr.ensure(static_cast<size_t>(nloc + 1) * 8);
+    op->col.ensure(std::max<size_t>(col.size(), 1) * 4);
+    op->vals.ensure(std::max<size_t>(static_cast<size_t>(op->nnz_local), 1) * 8);
+    KB_CUDA(cudaMemcpyAsync(op->row_ptr.p, rp, static_cast<size_t>(nloc + 1) * 8, cudaMemcpyHostToDevice, ctx.stream));
+    if (!col.empty()) {
+        KB_CUDA(cudaMemcpyAsync(op->col.p, col.data(), col.size() * 4, cudaMemcpyHostToDevice, ctx.stream));
+        KB_CUDA(cudaMemcpyAsync(op->vals.p, v, static_cast<size_t>(op->nnz_local) * 8, cudaMemcpyHostToDevice,
+                                ctx.stream));
+    }
+    if (ctx.nranks > 1) {
+        op->xfull.ensure(static_cast<size_t>(max_rows * ctx.nranks) * 8);
+        op->xsend.ensure(static_cast<size_t>(std::max<i64>(max_rows, 1)) * 8);
+    }
+    op->partials.ensure(static_cast<size_t>(reduce_grid() + 64) * 8);
+    ctx.sync();  // host vectors above go out of scope
+    return op;
+}
+
+int Operator::apply(const double* x, double* y, const double* b) {
+    Ctx& c = *ctx;
+    double* part = partials.p;
+    if (kind == CSR) {
+        const double* xs = x;
+        if (c.nranks > 1) {
+            KB_CUDA(cudaMemcpyAsync(xsend.p, x, static_cast<size_t>(nloc) * 8, cudaMemcpyDeviceToDevice, c.stream));
+            KB_NCCL(ncclAllGather(xsend.p, xfull.p, static_cast<size_t>(max_rows), ncclDouble, c.comm, c.stream));
+            xs = xfull.p;
+        }
+        return launch_csr(c.stream, nloc, row_ptr.as<int64_t>(), col.as<int32_t>(), vals.p, xs, b, y, part,
+                          c.launches);
+    }
+    if (c.nranks > 1) {
+        const i64 h = geom.halo;
+        KB_NCCL(ncclGroupStart());
+        if (c.rank > 0) {
+            KB_NCCL(ncclSend(x, static_cast<size_t>(h), ncclDouble, c.rank - 1, c.comm, c.stream));
+            KB_NCCL(ncclRecv(halo_lo.p, static_cast<size_t>(h), ncclDouble, c.rank - 1, c.comm, c.stream));
+        }
+        if (c.rank + 1 < c.nranks) {
+            KB_NCCL(ncclSend(x + nloc - h, static_cast<size_t>(h), ncclDouble, c.rank + 1, c.comm, c.stream));
+            KB_NCCL(ncclRecv(halo_hi.p, static_cast<size_t>(h), ncclDouble, c.rank + 1, c.comm, c.stream));
+        }
+        KB_NCCL(ncclGroupEnd());
+    }
+    return launch_stencil(c.stream, geom, x, halo_lo.p, halo_hi.p, b, y, part, c.launches);
+}
+
+double Operator::bytes_per_apply() const {
+    if (kind == CSR) return 12.0 * nnz_local + 8.0 * (nloc + 1) + 16.0 * nloc;
+    return 16.0 * nloc;
+}
+
+}  // namespace kb

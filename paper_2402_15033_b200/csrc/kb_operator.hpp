@@ -1,0 +1,37 @@
+// Device operators: CSR (krylov::CsrMatrix, csr_matrix.hpp:17-65) and the
+// matrix-free 5/7-point Laplacians that reproduce gen_laplace2d/3d
+// (matgen.hpp:134-187).  Rows are partitioned contiguously across the
+// context's ranks; apply() performs the halo exchange
+// over NCCL send/recv (NVLink P2P) before the row kernel.
+#pragma once
+
+#include "kb_ctx.hpp"
+#include "kb_kernels.hpp"
+
+namespace kb {
+
+struct Operator {
+    enum Kind { CSR = 0, LAPLACE2D = 1, LAPLACE3D = 2 };
+    Ctx* ctx = nullptr;
+    Kind kind = CSR;
+    i64 n_global = 0, row_begin = 0, nloc = 0, nnz_local = 0;
+    StencilGeom geom{};
+    DevBuf halo_lo, halo_hi;  // stencil halos (geom.halo doubles each)
+    // CSR
+    DevBuf row_ptr, col, vals;
+    DevBuf xfull, xsend;      // multi-rank gather of x
+    i64 max_rows = 0;
+    DevBuf partials;          // Σr² partials of the residual mode
+
+    // y = A·x (b == nullptr) or y = b − A·x with Σy² partials in `partials`;
+    // returns the number of partials written (0 without b).
+    int apply(const double* x, double* y, const double* b = nullptr);
+    // bytes moved by one application (algorithmic)
+    double bytes_per_apply() const;
+};
+
+Operator* make_laplace(Ctx& ctx, int dims, i64 nx, i64 ny, i64 nz);
+Operator* make_csr(Ctx& ctx, i64 n_global, i64 row_begin, i64 nloc, const int64_t* row_ptr,
+                   const int64_t* col_idx, const double* vals);
+
+}  // namespace kb

@@ -1,0 +1,126 @@
+#include "kb_ortho.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+#include "kb_kernels.hpp"
+
+namespace kb {
+
+namespace {
+
+std::vector<std::pair<i64, i64>> groups_for(i64 c0, i64 w) {
+    if (c0 == 0) {
+        if (round_up(w, 8) > 64)
+            fail(KRY_UNSUPPORTED, "block width above 64 columns is not supported on the device path");
+        return {{0, 0}};
+    }
+    return prefix_groups(c0, w);
+}
+
+}  // namespace
+
+void gram_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
+                 Mat& r_col, Mat& g) {
+    dim_check(w >= 1, "gram of empty matrix");
+    const auto groups = groups_for(c0, w);
+    ctx.gram_partials.ensure(static_cast<size_t>(gram_scratch_doubles(w)) * 8);
+    ctx.gram_packed.ensure(groups.size() * 64 * 64 * 8);
+    std::vector<std::vector<int>> tiles(groups.size());
+
+    cudaEvent_t t0 = ctx.begin_phase();
+    size_t offset = 0;
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const i64 start = groups[gi].first, cp = groups[gi].second;
+        launch_gram_pass(ctx.stream, n, cp > 0 ? P + start * ldp : nullptr, ldp, cp, V, ldv, w, gi == 0,
+                         ctx.gram_partials.p, ctx.gram_packed.p + offset, tiles[gi], ctx.launches);
+        offset += tiles[gi].size() * 64;
+    }
+    ctx.end_phase(PH_GRAM, t0);
+    ctx.gram_bytes += 8.0 * n * (c0 + w);
+    ctx.gram_launches += 1;
+    ctx.allreduce_sum(ctx.gram_packed.p, offset);
+    ctx.h_packed.ensure(std::max<size_t>(offset, 1) * 8);
+    KB_CUDA(cudaMemcpyAsync(ctx.h_packed.p, ctx.gram_packed.p, offset * 8, cudaMemcpyDeviceToHost, ctx.stream));
+    ctx.sync();
+
+    // Unpack: tile (jb, ib) entry e = m + 8·nn ↦ slot row 8ib+m, V column 8jb+nn.
+    const i64 wslots = round_up(w, 8);
+    r_col = Mat(c0, w);
+    g = Mat(w, w);
+    const double* h = ctx.h_packed.p;
+    size_t off = 0;
+    for (size_t gi = 0; gi < groups.size(); ++gi) {
+        const i64 start = groups[gi].first, cp = groups[gi].second;
+        for (int id : tiles[gi]) {
+            const int jb = id / 8, ib = id % 8;
+            for (int e = 0; e < 64; ++e) {
+                const i64 mrow = 8 * ib + (e & 7), j = 8 * jb + (e >> 3);
+                const double val = h[off + e];
+                if (j >= w) continue;
+                if (mrow < wslots) {
+                    if (mrow <= j) g(mrow, j) = val;
+                } else {
+                    const i64 l = mrow - wslots;
+                    if (l < cp) r_col(start + l, j) = val;
+                }
+            }
+            off += 64;
+        }
+    }
+    for (i64 j = 0; j < w; ++j)
+        for (i64 i = 0; i < j; ++i) g(j, i) = g(i, j);
+}
+
+void update_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
+                   const Mat& r_col, const Upper& r_jj, double* out, i64 ldo, bool triangular) {
+    if (triangular)
+        for (i64 j = 0; j < w; ++j)
+            if (r_jj(j, j) == 0.0) fail(KRY_SINGULAR_FACTOR, "triangular factor has a zero diagonal entry");
+    if (round_up(w, 8) > 64)
+        fail(KRY_UNSUPPORTED, "block width above 64 columns is not supported on the device path");
+    const int wmax = update_wmax(w);
+    const size_t total = static_cast<size_t>(c0 + wmax + 1) * wmax;
+    ctx.h_coef.ensure(total * 8);
+    ctx.coef.ensure(total * 8);
+    double* hc = ctx.h_coef.p;
+    std::memset(hc, 0, total * 8);
+    for (i64 l = 0; l < c0; ++l)
+        for (i64 j = 0; j < w; ++j) hc[l * wmax + j] = -r_col(l, j);
+    double* nrjj = hc + c0 * wmax;
+    double* inv = nrjj + static_cast<size_t>(wmax) * wmax;
+    for (i64 j = 0; j < w; ++j) {
+        for (i64 l = 0; l < j; ++l) nrjj[l * wmax + j] = triangular ? -r_jj(l, j) : 0.0;
+        inv[j] = triangular ? 1.0 / r_jj(j, j) : 1.0;
+    }
+    cudaEvent_t t0 = ctx.begin_phase();
+    KB_CUDA(cudaMemcpyAsync(ctx.coef.p, hc, total * 8, cudaMemcpyHostToDevice, ctx.stream));
+    launch_update(ctx.stream, n, c0 > 0 ? P : nullptr, ldp, c0, V, ldv, w, ctx.coef.p, triangular, out, ldo,
+                  ctx.launches);
+    ctx.end_phase(PH_UPDATE, t0);
+    ctx.update_bytes += 8.0 * n * (c0 + 2.0 * w);
+    ctx.update_launches += 1;
+}
+
+PipOut bcgs_pip_partial_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V,
+                               i64 ldv, i64 w, double* out, i64 ldo, i64& reduces) {
+    PipOut o;
+    reduces += 1;  // fused [Q_prev, V]ᵀV (block_ortho.hpp:155)
+    Mat s;
+    gram_device(ctx, n, P, ldp, c0, V, ldv, w, o.r_col, s);
+    if (c0 > 0) {
+        // Pythagorean update S = VᵀV − R_colᵀR_col, upper + mirror (block_ortho.hpp:159-166).
+        for (i64 j = 0; j < w; ++j)
+            for (i64 i = 0; i <= j; ++i) {
+                const double c = dot_seq(o.r_col.col(i), o.r_col.col(j), c0);
+                s(i, j) -= c;
+                if (i != j) s(j, i) = s(i, j);
+            }
+    }
+    o.bad_pivot = try_cholesky(s, o.r_jj);
+    if (o.bad_pivot != 0) return o;
+    update_device(ctx, n, P, ldp, c0, V, ldv, w, o.r_col, o.r_jj, out, ldo);
+    return o;
+}
+
+}  // namespace kb

@@ -1,0 +1,369 @@
+#include "kb_store.hpp"
+
+#include <algorithm>
+#include <cstring>
+
+#include "kb_ortho.hpp"
+
+namespace kb {
+
+Store::Store(Ctx& ctx, i64 n, i64 m, i64 panel_size, i64 big_panel_size)
+    : ctx_(ctx),
+      n_(n),
+      max_cols_(m + 1),
+      panel_size_(panel_size),
+      big_panel_size_(big_panel_size == 0 ? m : big_panel_size),
+      ld_(device_ld(n)),
+      r_(m + 1) {
+    // BasisStore ctor checks (basis_store.hpp:51-54).
+    if (panel_size_ == 0 || m % panel_size_ != 0)
+        fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: panel size must divide the restart length");
+    if (big_panel_size_ % panel_size_ != 0 || big_panel_size_ > m)
+        fail(KRY_DIMENSION_MISMATCH,
+             "dimension mismatch: big panel size must be a multiple of the panel size, <= m");
+    q_.ensure(static_cast<size_t>(ld_) * max_cols_ * 8);
+    KB_CUDA(cudaMemsetAsync(q_.p, 0, static_cast<size_t>(ld_) * max_cols_ * 8, ctx_.stream));
+}
+
+void Store::reset() {
+    filled_ = 0;
+    finalized_ = 0;
+    big_panel_start_ = 0;
+    seam_valid_ = false;
+    states_.clear();
+    records_.clear();
+    r_ = Upper(max_cols_);
+    // The reference also zeroes Q (basis_store.hpp:91).  The solver never
+    // reads a column before writing it, so gmres() skips this pass
+    // (Store::reset is only used by the C-ABI reset, where it is kept).
+}
+
+void Store::seed_unit_column(const double* d_v) {
+    if (filled_ != 0) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: seed requires an empty store");
+    if (d_v != col(0))
+        KB_CUDA(cudaMemcpyAsync(col(0), d_v, static_cast<size_t>(n_) * 8, cudaMemcpyDeviceToDevice, ctx_.stream));
+    r_.at(0, 0) = 1.0;
+    filled_ = 1;
+    finalized_ = 1;
+    big_panel_start_ = 1;
+}
+
+double* Store::scratch(int which, i64 w) {
+    scratch_[which].ensure(static_cast<size_t>(ld_) * round_up(w, 8) * 8);
+    return scratch_[which].p;
+}
+
+void Store::mpk(Operator& op, i64 c0, i64 s) {
+    dim_check(c0 + s + 1 <= max_cols_, "basis store capacity exceeded");
+    for (i64 k = 0; k < s; ++k) op.apply(col(c0 + k), col(c0 + k + 1));
+}
+
+Outcome Store::append_block(const double* V, i64 ldv, i64 w, bool overlap, int kind, i64, Sync& sync) {
+    const i64 before = sync.reduces;
+    Outcome out = append_impl(V, ldv, w, overlap, kind, sync);
+    sync.per_block.push_back(sync.reduces - before);
+    return out;
+}
+
+Outcome Store::preprocess_block(const double* V, i64 ldv, i64 w, bool overlap, Sync& sync) {
+    return append_block(V, ldv, w, overlap, KRY_ORTHO_TWO_STAGE, big_panel_size_, sync);
+}
+
+Outcome Store::append_impl(const double* V, i64 ldv, i64 w, bool overlap, int kind, Sync& sync) {
+    Outcome out;
+    i64 width = w;
+    if (overlap && filled_ == 0) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: basis store capacity exceeded");
+    const i64 c0 = overlap ? filled_ - 1 : filled_;
+    if (c0 + width > max_cols_) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: basis store capacity exceeded");
+
+    // basis_store.hpp:178-208: first-pass pivot failure truncates and retries.
+    while (width >= 1) {
+        i64 bad = 0;
+        try {
+            OrthoRes res = run_scheme(c0, V, ldv, width, kind, sync);
+            commit(c0, overlap, res, width, kind == KRY_ORTHO_TWO_STAGE ? KRY_PANEL_PREPROCESSED : KRY_PANEL_FINAL);
+            out.committed = width;
+            if (out.truncated) record_seam(V + width * ldv, sync);
+            return out;
+        } catch (const FirstPassFailure& e) {
+            bad = e.pivot;
+        } catch (const SecondPassBreakdown& e) {
+            out.breakdown = true;
+            out.truncated = false;
+            out.pivot = e.pivot;
+            out.kappa_estimate = diagnostic_kappa(c0, V, ldv, width);
+            return out;
+        }
+        out.truncated = true;
+        out.pivot = bad;
+        if (bad <= 1) break;
+        width = std::min(width, bad - 1);
+    }
+    out.breakdown = true;
+    out.truncated = false;
+    out.kappa_estimate = diagnostic_kappa(c0, V, ldv, w);
+    return out;
+}
+
+Store::OrthoRes Store::pip(i64 c0, const double* V, i64 ldv, i64 w, double* out, i64 ldo, Sync& sync,
+                           bool first_pass) {
+    i64 red = 0;
+    PipOut o = bcgs_pip_partial_device(ctx_, n_, col(0), ld_, c0, V, ldv, w, out, ldo, red);
+    sync.add(red);
+    ortho_bytes += 8.0 * n_ * (2.0 * c0 + 3.0 * w);
+    if (o.bad_pivot != 0) {
+        if (first_pass) throw FirstPassFailure{o.bad_pivot};
+        throw SecondPassBreakdown{o.bad_pivot};
+    }
+    return OrthoRes{std::move(o.r_col), std::move(o.r_jj)};
+}
+
+namespace {
+
+// CholQR (block_ortho.hpp:49-54) on the device: one reduce.  Throws
+// `Fail{pivot}` on a Cholesky failure (the caller maps it to the reference's
+// first/second-pass semantics).
+struct CholFail {
+    i64 pivot;
+};
+
+Upper cholqr_device(Ctx& ctx, i64 n, const double* V, i64 ldv, i64 w, double* out, i64 ldo, Sync& sync,
+                    double& bytes) {
+    sync.add(1);
+    Mat none, g;
+    gram_device(ctx, n, nullptr, 0, 0, V, ldv, w, none, g);
+    Upper r;
+    const i64 piv = try_cholesky(g, r);
+    if (piv != 0) throw CholFail{piv};
+    update_device(ctx, n, nullptr, 0, 0, V, ldv, w, none, r, out, ldo);
+    bytes += 8.0 * n * 3.0 * w;
+    return r;
+}
+
+// bcgs_project (block_ortho.hpp:70-87): one reduce when the prefix is non-empty.
+Mat project_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
+                   double* out, i64 ldo, Sync& sync, double& bytes) {
+    if (c0 == 0) {
+        if (out != V)
+            KB_CUDA(cudaMemcpy2DAsync(out, ldo * 8, V, ldv * 8, n * 8, w, cudaMemcpyDeviceToDevice, ctx.stream));
+        return Mat(0, w);
+    }
+    sync.add(1);
+    Mat r_block, g;
+    gram_device(ctx, n, P, ldp, c0, V, ldv, w, r_block, g);
+    Upper ident(w);
+    update_device(ctx, n, P, ldp, c0, V, ldv, w, r_block, ident, out, ldo, /*triangular=*/false);
+    bytes += 8.0 * n * (2.0 * c0 + 3.0 * w);
+    return r_block;
+}
+
+}  // namespace
+
+Store::OrthoRes Store::run_scheme(i64 c0, const double* V, i64 ldv, i64 w, int kind, Sync& sync) {
+    switch (kind) {
+        case KRY_ORTHO_TWO_STAGE:
+            return pip(c0, V, ldv, w, col(c0), ld_, sync, true);  // single first-stage pass
+        case KRY_ORTHO_BCGS_PIP2: {
+            double* s0 = scratch(0, w);
+            OrthoRes first = pip(c0, V, ldv, w, s0, ld_, sync, true);
+            OrthoRes second = pip(c0, s0, ld_, w, col(c0), ld_, sync, false);
+            OrthoRes out;
+            out.r_col = std::move(first.r_col);
+            if (out.r_col.rows > 0) {
+                Mat rjj(w, w);
+                for (i64 j = 0; j < w; ++j)
+                    for (i64 i = 0; i <= j; ++i) rjj(i, j) = first.r_jj(i, j);
+                Mat corr = mat_mul_nn(second.r_col, rjj);
+                for (i64 j = 0; j < out.r_col.cols; ++j)
+                    for (i64 i = 0; i < out.r_col.rows; ++i) out.r_col(i, j) += corr(i, j);
+            }
+            out.r_jj = tri_mul(second.r_jj, first.r_jj);
+            return out;
+        }
+        case KRY_ORTHO_BCGS2_HHQR:
+        case KRY_ORTHO_BCGS2_CHOLQR2: {
+            // bcgs2 (block_ortho.hpp:102-137) / run_scheme (basis_store.hpp:240-280).
+            const bool single = (w == 1);
+            if (kind == KRY_ORTHO_BCGS2_HHQR && !single)
+                fail(KRY_UNSUPPORTED, "BCGS2 with a Householder intra step is not on the device path");
+            double* s0 = scratch(0, w);
+            double* s1 = scratch(1, w);
+            // intra: CholQR (single column) or CholQR2; input x → output dst.
+            auto intra = [&](const double* x, i64 ldx, double* dst) -> Upper {
+                if (single) return cholqr_device(ctx_, n_, x, ldx, w, dst, ld_, sync, ortho_bytes);
+                Upper r1 = cholqr_device(ctx_, n_, x, ldx, w, dst, ld_, sync, ortho_bytes);
+                Upper r2 = cholqr_device(ctx_, n_, dst, ld_, w, dst, ld_, sync, ortho_bytes);
+                return tri_mul(r2, r1);
+            };
+            OrthoRes out;
+            if (c0 == 0) {
+                try {
+                    out.r_jj = intra(V, ldv, col(c0));
+                } catch (const CholFail& f) {
+                    throw FirstPassFailure{f.pivot};
+                }
+                out.r_col = Mat(0, w);
+                return out;
+            }
+            Mat first_block;
+            Upper inner_r;
+            try {
+                first_block = project_device(ctx_, n_, col(0), ld_, c0, V, ldv, w, s0, ld_, sync, ortho_bytes);
+                inner_r = intra(s0, ld_, s1);
+            } catch (const CholFail& f) {
+                throw FirstPassFailure{f.pivot};
+            }
+            try {
+                Mat second_block =
+                    project_device(ctx_, n_, col(0), ld_, c0, s1, ld_, w, s1, ld_, sync, ortho_bytes);
+                Upper outer_r = cholqr_device(ctx_, n_, s1, ld_, w, col(c0), ld_, sync, ortho_bytes);
+                Mat ir(w, w);
+                for (i64 j = 0; j < w; ++j)
+                    for (i64 i = 0; i <= j; ++i) ir(i, j) = inner_r(i, j);
+                Mat corr = mat_mul_nn(second_block, ir);
+                out.r_col = std::move(first_block);
+                for (i64 j = 0; j < out.r_col.cols; ++j)
+                    for (i64 i = 0; i < out.r_col.rows; ++i) out.r_col(i, j) += corr(i, j);
+                out.r_jj = tri_mul(outer_r, inner_r);
+                return out;
+            } catch (const CholFail& f) {
+                throw SecondPassBreakdown{f.pivot};
+            }
+        }
+    }
+    fail(KRY_INVALID_ARGUMENT, "unknown orthogonalization scheme");
+}
+
+void Store::commit(i64 c0, bool overlap, const OrthoRes& res, i64 w, int state) {
+    // basis_store.hpp:285-327 (the q copy is unnecessary: run_scheme already
+    // wrote the block into columns [c0, c0+w)).
+    BlockRecord rec;
+    rec.c0 = c0;
+    rec.width = w;
+    rec.overlap = overlap;
+    const i64 rc = res.r_col.rows;
+    if (overlap) {
+        const double rho = r_(c0, c0);
+        if (rc > 0) rec.carried.assign(res.r_col.col(0), res.r_col.col(0) + c0);
+        rec.carried_diag = res.r_jj(0, 0);
+        for (i64 i = 0; i < c0; ++i) r_.at(i, c0) += rho * res.r_col(i, 0);
+        r_.at(c0, c0) = rho * res.r_jj(0, 0);
+        for (i64 j = 1; j < w; ++j) {
+            for (i64 i = 0; i < c0; ++i) r_.at(i, c0 + j) = res.r_col(i, j);
+            for (i64 i = 0; i <= j; ++i) r_.at(c0 + i, c0 + j) = res.r_jj(i, j);
+        }
+    } else {
+        for (i64 j = 0; j < w; ++j) {
+            for (i64 i = 0; i < c0; ++i) r_.at(i, c0 + j) = (rc > 0) ? res.r_col(i, j) : 0.0;
+            for (i64 i = 0; i <= j; ++i) r_.at(c0 + i, c0 + j) = res.r_jj(i, j);
+        }
+    }
+    filled_ = c0 + w;
+    seam_valid_ = false;
+    if (state == KRY_PANEL_FINAL) {
+        finalized_ = filled_;
+        big_panel_start_ = filled_;
+    } else {
+        big_panel_start_ = std::min(big_panel_start_, c0);
+        finalized_ = std::min(finalized_, c0);
+    }
+    states_.push_back(state);
+    records_.push_back(std::move(rec));
+}
+
+Outcome Store::finalize_big_panel(Sync& sync) {
+    const i64 before = sync.reduces;
+    Outcome out;
+    if (!big_panel_open()) return out;
+    const i64 c0 = big_panel_start_;
+    const i64 w = filled_ - c0;
+    OrthoRes res;
+    try {
+        res = pip(c0, col(c0), ld_, w, col(c0), ld_, sync, true);
+    } catch (const FirstPassFailure& e) {
+        out.breakdown = true;
+        out.pivot = e.pivot;
+        out.kappa_estimate = diagnostic_kappa(c0, col(c0), ld_, w);
+        sync.per_big_panel.push_back(sync.reduces - before);
+        return out;
+    }
+    for (i64 c = c0; c < filled_; ++c) combine_column(c, c0, w, res);
+    for (BlockRecord& rec : records_)
+        if (rec.c0 >= c0) combine_record(rec, c0, w, res);
+    finalized_ = filled_;
+    big_panel_start_ = filled_;
+    for (int& st : states_)
+        if (st == KRY_PANEL_PREPROCESSED) st = KRY_PANEL_FINAL;
+    out.committed = w;
+    sync.per_big_panel.push_back(sync.reduces - before);
+    return out;
+}
+
+void Store::combine_column(i64 c, i64 c0, i64 w, const OrthoRes& res) {
+    // basis_store.hpp:331-345
+    std::vector<double> part(static_cast<size_t>(w), 0.0);
+    const i64 top = std::min(c, c0 + w - 1);
+    for (i64 i = c0; i <= top; ++i) part[i - c0] = r_(i, c);
+    for (i64 i = 0; i < c0; ++i) {
+        double s = 0.0;
+        for (i64 l = 0; l < w; ++l) s += res.r_col(i, l) * part[l];
+        r_.at(i, c) += s;
+    }
+    for (i64 i = 0; i < w && c0 + i <= c; ++i) {
+        double s = 0.0;
+        for (i64 l = i; l < w; ++l) s += res.r_jj(i, l) * part[l];
+        r_.at(c0 + i, c) = s;
+    }
+}
+
+void Store::combine_record(BlockRecord& rec, i64 c0, i64 w, const OrthoRes& res) {
+    // basis_store.hpp:347-369.  Divergence: a
+    // non-overlap record with c0 > 0 has no carried column; the reference
+    // dereferences an empty vector there.  It is skipped (the solver never
+    // produces one: only block 0 is non-overlap and it has c0 = 0).
+    if (!rec.overlap && rec.c0 > 0) return;
+    std::vector<double> full(static_cast<size_t>(rec.c0 + 1), 0.0);
+    for (i64 i = 0; i < rec.c0; ++i) full[i] = rec.carried[i];
+    full[rec.c0] = rec.carried_diag;
+    std::vector<double> part(static_cast<size_t>(w), 0.0);
+    const i64 top = std::min(rec.c0, c0 + w - 1);
+    for (i64 i = c0; i <= top; ++i) part[i - c0] = full[i];
+    for (i64 i = 0; i < c0; ++i) {
+        double s = 0.0;
+        for (i64 l = 0; l < w; ++l) s += res.r_col(i, l) * part[l];
+        full[i] += s;
+    }
+    for (i64 i = 0; i < w && c0 + i <= rec.c0; ++i) {
+        double s = 0.0;
+        for (i64 l = i; l < w; ++l) s += res.r_jj(i, l) * part[l];
+        full[c0 + i] = s;
+    }
+    for (i64 i = 0; i < rec.c0; ++i) rec.carried[i] = full[i];
+    rec.carried_diag = full[rec.c0];
+}
+
+void Store::record_seam(const double* dropped, Sync& sync) {
+    // basis_store.hpp:374-381: coefficients of the first dropped raw vector.
+    if (filled_ >= max_cols_) return;
+    sync.add(1);
+    Mat rc, g;
+    gram_device(ctx_, n_, col(0), ld_, filled_, dropped, ld_, 1, rc, g);
+    for (i64 i = 0; i < filled_; ++i) r_.at(i, filled_) = rc(i, 0);
+    r_.at(filled_, filled_) = 0.0;
+    seam_valid_ = true;
+}
+
+double Store::diagnostic_kappa(i64 c0, const double* V, i64 ldv, i64 w) {
+    // basis_store.hpp:383-387 → accumulated_cond on host copies.  The
+    // diagnostic needs every row, so a multi-rank run reports 0.
+    if (c0 + w > 512 || ctx_.nranks > 1) return 0.0;
+    Mat q(n_, c0), x(n_, w);
+    if (c0 > 0)
+        KB_CUDA(cudaMemcpy2DAsync(q.a.data(), n_ * 8, col(0), ld_ * 8, n_ * 8, c0, cudaMemcpyDeviceToHost,
+                                  ctx_.stream));
+    KB_CUDA(cudaMemcpy2DAsync(x.a.data(), n_ * 8, V, ldv * 8, n_ * 8, w, cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+    return accumulated_cond(q, x);
+}
+
+}  // namespace kb

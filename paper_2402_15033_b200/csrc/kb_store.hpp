@@ -1,0 +1,105 @@
+// Device-resident basis store (krylov::BasisStore, basis_store.hpp:42-401).
+//
+// Q lives in HBM as one column-major n×(m+1) allocation (ld padded for TMA);
+// the MPK writes each block straight into its columns and BCGS-PIP rewrites
+// them in place, so a block never round-trips through a separate buffer.  R,
+// the block records and the panel state machine are host-side and follow
+// the reference operation for operation (they are O(m²) and replicated per
+// rank).
+#pragma once
+
+#include <vector>
+
+#include "kb_ctx.hpp"
+#include "kb_dense.hpp"
+#include "kb_operator.hpp"
+
+namespace kb {
+
+struct Sync {  // SyncCounter (block_ortho.hpp:15-21)
+    i64 reduces = 0;
+    std::vector<i64> per_block, per_big_panel;
+    void add(i64 k = 1) { reduces += k; }
+};
+
+struct Outcome {  // AppendOutcome (basis_store.hpp:16-22)
+    i64 committed = 0;
+    bool truncated = false;
+    bool breakdown = false;
+    i64 pivot = 0;
+    double kappa_estimate = 0.0;
+};
+
+class Store {
+public:
+    Store(Ctx& ctx, i64 n, i64 m, i64 panel_size, i64 big_panel_size);
+
+    i64 rows() const { return n_; }
+    i64 capacity() const { return max_cols_; }
+    i64 filled() const { return filled_; }
+    i64 finalized_count() const { return finalized_; }
+    i64 big_panel_start() const { return big_panel_start_; }
+    i64 panel_size() const { return panel_size_; }
+    i64 big_panel_size() const { return big_panel_size_; }
+    bool big_panel_open() const { return filled_ > big_panel_start_; }
+    bool big_panel_full() const { return big_panel_open() && filled_ - big_panel_start_ >= big_panel_size_ + 1; }
+    bool has_seam_column() const { return seam_valid_; }
+    const Upper& coefficients() const { return r_; }
+    const std::vector<int>& panel_states() const { return states_; }
+    const std::vector<BlockRecord>& block_records() const { return records_; }
+    double* col(i64 j) { return q_.p + j * ld_; }
+    const double* col(i64 j) const { return q_.p + j * ld_; }
+    i64 ld() const { return ld_; }
+    Ctx& ctx() { return ctx_; }
+
+    void reset();
+    void zero_q() { KB_CUDA(cudaMemsetAsync(q_.p, 0, q_.bytes, ctx_.stream)); }
+    void seed_unit_column(const double* d_v);
+    // V (device, n×w, leading dimension ldv) may be the store's own columns
+    // [c0, c0+w) (in-place path used by the solver's MPK) or a caller buffer.
+    Outcome append_block(const double* V, i64 ldv, i64 w, bool overlap, int kind, i64 big_panel,
+                         Sync& sync);
+    Outcome preprocess_block(const double* V, i64 ldv, i64 w, bool overlap, Sync& sync);
+    Outcome finalize_big_panel(Sync& sync);
+    // MPK into the store: column c0 holds the start; columns c0+1..c0+s.
+    void mpk(Operator& op, i64 c0, i64 s);
+
+    // Telemetry: algorithmic BlkOrtho bytes for this rank.
+    double ortho_bytes = 0.0;
+
+private:
+    struct OrthoRes {
+        Mat r_col;
+        Upper r_jj;
+    };
+    struct SecondPassBreakdown {
+        i64 pivot;
+    };
+    struct FirstPassFailure {
+        i64 pivot;
+    };
+
+    Outcome append_impl(const double* V, i64 ldv, i64 w, bool overlap, int kind, Sync& sync);
+    // Writes the orthonormal block into store columns [c0, c0+w).
+    OrthoRes run_scheme(i64 c0, const double* V, i64 ldv, i64 w, int kind, Sync& sync);
+    OrthoRes pip(i64 c0, const double* V, i64 ldv, i64 w, double* out, i64 ldo, Sync& sync, bool first_pass);
+    void commit(i64 c0, bool overlap, const OrthoRes& res, i64 w, int state);
+    void combine_column(i64 col, i64 c0, i64 w, const OrthoRes& res);
+    void combine_record(BlockRecord& rec, i64 c0, i64 w, const OrthoRes& res);
+    void record_seam(const double* dropped, Sync& sync);
+    double diagnostic_kappa(i64 c0, const double* V, i64 ldv, i64 w);
+    double* scratch(int which, i64 w);
+
+    Ctx& ctx_;
+    i64 n_, max_cols_, panel_size_, big_panel_size_;
+    i64 filled_ = 0, finalized_ = 0, big_panel_start_ = 0;
+    bool seam_valid_ = false;
+    DevBuf q_;
+    i64 ld_;
+    Upper r_;
+    std::vector<int> states_;
+    std::vector<BlockRecord> records_;
+    DevBuf scratch_[2];
+};
+
+}  // namespace kb

@@ -1,0 +1,192 @@
+"""Kernel-level parity of the CUDA path against the CPU reference (oracle/_ref).
+
+Protocol: SpMV/stencil bit-exact; Gram / BCGS-PIP outputs
+within 1e-12 relative (Frobenius) of the reference on identical inputs;
+Cholesky pivot outcomes identical.
+"""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def rel(a, b):
+    a, b = np.asarray(a), np.asarray(b)
+    d = np.linalg.norm(a - b)
+    s = max(np.linalg.norm(b), 1e-300)
+    return d / s
+
+
+# ---- K1/K2: SpMV and MPK (spmv csr_matrix.hpp:69, mpk_monomial gmres.hpp:80) ----------
+@pytest.mark.parametrize("nx,ny", [(2, 2), (3, 7), (12, 12), (100, 37), (512, 512)])
+def test_laplace2d_stencil_bitwise(kb, ctx, ref, rng, nx, ny):
+    a = ref.laplace2d(nx, ny)
+    op = kb.Laplace2D(nx, ny)
+    assert op.n == a.n
+    x = rng.standard_normal(a.n)
+    np.testing.assert_array_equal(op.spmv(x), ref.spmv(a, x))
+
+
+@pytest.mark.parametrize("dims", [(2, 2, 2), (5, 3, 4), (17, 9, 11), (64, 64, 64)])
+def test_laplace3d_stencil_bitwise(kb, ctx, ref, rng, dims):
+    a = ref.laplace3d(*dims)
+    op = kb.Laplace3D(*dims)
+    x = rng.standard_normal(a.n)
+    np.testing.assert_array_equal(op.spmv(x), ref.spmv(a, x))
+
+
+def random_csr(rng, n, per_row):
+    rows = []
+    for i in range(n):
+        cols = np.unique(np.concatenate([[i], rng.integers(0, n, per_row)]))
+        vals = rng.standard_normal(cols.size)
+        vals[cols == i] += 4.0
+        rows.append((cols, vals))
+    rp = np.zeros(n + 1, np.int64)
+    rp[1:] = np.cumsum([c.size for c, _ in rows])
+    ci = np.concatenate([c for c, _ in rows]).astype(np.int64)
+    vv = np.concatenate([v for _, v in rows])
+    return rp, ci, vv
+
+
+@pytest.mark.parametrize("n,per_row", [(1, 0), (40, 3), (1000, 7), (20000, 30)])
+def test_csr_spmv_bitwise(kb, ctx, ref, rng, n, per_row):
+    rp, ci, vv = random_csr(rng, n, per_row)
+    a = ref.Csr(n, rp, ci, vv)
+    op = kb.CsrOperator(rp, ci, vv)
+    x = rng.standard_normal(n)
+    np.testing.assert_array_equal(op.spmv(x), ref.spmv(a, x))
+
+
+def test_csr_laplace_matches_stencil(kb, ctx, ref, rng):
+    a = ref.laplace2d(33, 21)
+    csr = kb.CsrOperator(a.row_ptr, a.col_idx, a.vals)
+    st = kb.Laplace2D(33, 21)
+    x = rng.standard_normal(a.n)
+    np.testing.assert_array_equal(csr.spmv(x), st.spmv(x))
+
+
+@pytest.mark.parametrize("s", [1, 3, 5])
+def test_mpk_bitwise(kb, ctx, ref, rng, s):
+    a = ref.laplace2d(40, 30)
+    op = kb.Laplace2D(40, 30)
+    start = rng.standard_normal(a.n)
+    start /= np.linalg.norm(start)
+    np.testing.assert_array_equal(op.mpk(start, s), ref.mpk(a, start, s))
+
+
+def test_spmv_rejects_bad_length(kb, ctx):
+    op = kb.Laplace2D(4, 4)
+    with pytest.raises(kb.DimensionMismatch):
+        op.spmv(np.ones(15))
+
+
+def test_operator_dimension_errors(kb, ctx):
+    with pytest.raises(kb.DimensionMismatch):
+        kb.Laplace2D(1, 5)
+    with pytest.raises(kb.DimensionMismatch):
+        kb.Laplace3D(2, 2, 1)
+
+
+# ---- K3: fused Gram [Q_prev V]ᵀV ---------------------------------------------------------
+SHAPES = [(0, 1), (0, 6), (5, 6), (17, 3), (55, 6), (0, 21), (20, 21), (40, 21), (0, 31), (30, 31),
+          (50, 11), (0, 61), (3, 61 - 3 - 1), (100, 6), (45, 16)]
+
+
+@pytest.mark.parametrize("c0,w", SHAPES)
+@pytest.mark.parametrize("n", [7, 1000, 100003])
+def test_gram_matches_reference(kb, ctx, ref, rng, n, c0, w):
+    if c0 > 0 and (w + 7) // 8 * 8 > 56:
+        pytest.skip("shape outside the device envelope (w ≤ 56 with a prefix)")
+    q = rng.standard_normal((n, c0))
+    v = rng.standard_normal((n, w))
+    rc, g = kb.gram(q if c0 else None, v)
+    g_ref = ref.gram(v)
+    assert rel(g, g_ref) < 1e-13
+    np.testing.assert_array_equal(g, g.T)  # mirrored bit-exactly, like gram()
+    if c0:
+        assert rel(rc, ref.mat_mul_tn(q, v)) < 1e-13
+
+
+def test_gram_deterministic(kb, ctx, rng):
+    v = rng.standard_normal((300001, 6))
+    q = rng.standard_normal((300001, 25))
+    a = kb.gram(q, v)
+    b = kb.gram(q, v)
+    np.testing.assert_array_equal(a[0], b[0])
+    np.testing.assert_array_equal(a[1], b[1])
+
+
+# ---- K4/K5: BCGS-PIP (block_ortho.hpp:152-189) -------------------------------------------
+def orthonormal(rng, n, k):
+    q, _ = np.linalg.qr(rng.standard_normal((n, k)))
+    return np.asfortranarray(q)
+
+
+@pytest.mark.parametrize("n,c0,w", [(120, 0, 5), (500, 6, 4), (4000, 55, 6), (20000, 0, 61), (20000, 40, 21),
+                                    (5000, 50, 11), (100003, 25, 6)])
+def test_bcgs_pip_matches_reference(kb, ctx, ref, rng, n, c0, w):
+    q = orthonormal(rng, n, c0) if c0 else None
+    v = rng.standard_normal((n, w))
+    sync = kb.SyncCounter()
+    res = kb.bcgs_pip(q, v, sync)
+    q_ref, rc_ref, rj_ref, red = ref.bcgs_pip(q, v)
+    assert sync.reduces == red == 1
+    assert rel(res.q, q_ref) < 1e-12
+    assert rel(res.r_jj, rj_ref) < 1e-12
+    if c0:
+        assert rel(res.r_col, rc_ref) < 1e-12
+    assert np.all(np.diag(res.r_jj) > 0)
+
+
+def test_bcgs_pip_empty_prefix_is_cholqr(kb, ctx, rng):
+    # BcgsPip.EmptyPrefixIsCholQrBitwise (tests/test_block_ortho.cpp:172-181)
+    v = rng.standard_normal((120, 5))
+    s1, s2 = kb.SyncCounter(), kb.SyncCounter()
+    pip = kb.bcgs_pip(None, v, s1)
+    chol = kb.cholqr(v, s2)
+    np.testing.assert_array_equal(pip.q, chol.q)
+    np.testing.assert_array_equal(np.triu(pip.r_jj), np.triu(chol.r))
+    assert s1.reduces == 1
+
+
+def test_bcgs_pip_rank_deficient_pivot(kb, ctx, ref, rng):
+    v = rng.standard_normal((300, 4))
+    v[:, 2] = 0.0  # exact zero column: pivot 3 fails for any reduction order
+    sync = kb.SyncCounter()
+    with pytest.raises(kb.NotPositiveDefinite) as e:
+        kb.bcgs_pip(None, v, sync)
+    with pytest.raises(ref.RefError) as er:
+        ref.bcgs_pip(None, v)
+    assert e.value.pivot == er.value.pivot == 3
+    assert sync.reduces == 1
+
+
+def test_bcgs_pip2_glued_matches_reference(kb, ctx, ref):
+    # BcgsPip2.GluedWithinRangeStaysOrthogonal (tests/test_block_ortho.cpp:199-214)
+    n, s, p = 20000, 5, 4
+    glued = ref.gen_glued(n, p, s, 1e7, 1.0, 0.1, 16)
+    sync = kb.SyncCounter()
+    q_acc = np.zeros((n, 0), order="F")
+    q_ref = np.zeros((n, 0), order="F")
+    for j in range(p):
+        blk = glued[:, j * s:(j + 1) * s]
+        res = kb.bcgs_pip2(q_acc if q_acc.shape[1] else None, blk, sync)
+        rq, rrc, rrj, _ = ref.bcgs_pip2(q_ref if q_ref.shape[1] else None, blk)
+        assert rel(res.q, rq) < 1e-9
+        q_acc = np.asfortranarray(np.hstack([q_acc, res.q]))
+        q_ref = np.asfortranarray(np.hstack([q_ref, rq]))
+    assert sync.reduces == 2 * p
+    assert ref.ortho_error(q_acc) < 1e-13
+
+
+def test_pip_partial_reports_partial_factor(kb, ctx, ref, rng):
+    q = orthonormal(rng, 800, 6)
+    v = rng.standard_normal((800, 5))
+    v[:, 3] = 0.0  # zero column: the Pythagorean pivot 4 is exactly 0
+    sync = kb.SyncCounter()
+    out = kb.bcgs_pip_partial(q, v, sync)
+    _, rc, rj, piv, _ = ref.bcgs_pip_partial(q, v)
+    assert out.bad_pivot == piv
+    assert out.q is None
+    assert rel(out.r_col, rc) < 1e-12

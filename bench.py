@@ -1,0 +1,399 @@
+#!/usr/bin/env python
+"""Benchmark of the B200 two-stage s-step GMRES hot path (BASELINE.json metric).
+
+Workload (BASELINE.json configs[1]): 2D Laplace 5-point, 4000×4000 rows per
+GPU (weak scaling: the grid is 4000 × 4000·N for N ranks, row-partitioned by
+whole grid lines), b = A·1, s-step GMRES(60), s = 5, two-stage BlkOrtho with
+ŝ = 60, fp64.  One timed *step* = one full restart cycle through the C ABI
+(kry_sstep_gmres_device with max_iters = 60, warm-started from the current x):
+12 MPK blocks (60 stencil SpMVs), 12 first-stage BCGS-PIP, 1 second-stage
+BCGS-PIP finalize of the 61-column big panel, Hessenberg/LSQ, solution update
+and explicit residual.  Inputs live in HBM (the 7.8 GB/GPU basis is ≫ the
+126 MB L2, so no L2 flush is needed between steps).
+
+`value` = aggregate BlkOrtho HBM GB/s: Σ_ranks algorithmic BlkOrtho bytes
+(8·n·(2c0+3w) per BCGS-PIP) ÷ BlkOrtho device time (CUDA events
+on the solver stream around Gram + allreduce + Cholesky + update, max over
+ranks).  `e2e` = the same bytes ÷ the end-to-end wall time of the same cycles
+through the host-buffer C ABI (kry_sstep_gmres: b and x0 copied H2D from
+pinned memory, x copied D2H, every step).
+
+  python bench.py                      # N=1, 3 warm-up + 5 timed cycles
+  python bench.py --impl reference     # the CPU reference on the same config
+  torchrun --nproc-per-node N bench.py --gpus N
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GMRES time-to-solution (s) & BlkOrtho HBM GB/s, 2D Laplace, 1/2/4/8 B200"
+
+
+def parse():
+    p = argparse.ArgumentParser()
+    p.add_argument("--gpus", type=int, default=1)
+    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--warmup", type=int, default=3)
+    p.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    p.add_argument("--grid", type=int, default=4000, help="grid side per GPU (rows per GPU = grid²)")
+    p.add_argument("--shat", type=int, default=60)
+    p.add_argument("--scheme", choices=["two-stage", "bcgs-pip2"], default="two-stage")
+    p.add_argument("--tts", action="store_true", help="also measure a full time-to-solution solve (N=1)")
+    p.add_argument("--no-cpu-baseline", action="store_true")
+    p.add_argument("--no-e2e", action="store_true")
+    p.add_argument("--cpu-sample-blocks", type=int, default=3)
+    return p.parse_args()
+
+
+def peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    try:
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json copy test)"
+    except Exception:
+        return 6650.0, "fallback (B200_PROFILING.md)"
+
+
+class Clocks:
+    """nvidia-smi sampling during the timed region (B200_PROFILING.md clocks line)."""
+
+    FIELDS = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+              "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+              "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index):
+        self.gpu = gpu_index
+        self.proc = None
+        self.lines = []
+
+    def __enter__(self):
+        try:
+            self.proc = subprocess.Popen(
+                ["nvidia-smi", "-i", str(self.gpu), f"--query-gpu={self.FIELDS}", "--format=csv,noheader,nounits",
+                 "-lms", "200"], stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except Exception:
+            self.proc = None
+        return self
+
+    def __exit__(self, *a):
+        if self.proc is None:
+            return
+        self.proc.terminate()
+        try:
+            out, _ = self.proc.communicate(timeout=5)
+        except Exception:
+            self.proc.kill()
+            out, _ = self.proc.communicate()
+        self.lines = [l for l in out.splitlines() if l.strip()]
+
+    def summary(self):
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for l in self.lines:
+            f = [x.strip() for x in l.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for nm, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(nm)
+        if not sm:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        return {"sm_mhz": statistics.median(sm), "sm_max_mhz": max(mx), "reasons": sorted(reasons),
+                "samples": len(sm)}
+
+
+# ---------------------------------------------------------------------------------------
+def reference_blkortho_sample(grid, shat, blocks, threads, v_from_gpu=None):
+    """Time the CPU reference's BlkOrtho (BasisStore::preprocess_block) on the
+    first `blocks` blocks of a restart cycle at the bench config.  V blocks are
+    the reference's own MPK on its own CSR (or, for the cpu_baseline leg of our
+    arm, the bit-identical GPU MPK output when `v_from_gpu` is given).
+    Returns (GB/s, seconds, bytes, sample description)."""
+    os.environ["KRYLOV_NUM_THREADS"] = str(threads)
+    import numpy as np
+    from oracle import ref
+
+    n = grid * grid
+    m, s = 60, 5
+    st = ref.Store(n, m, s, shat)
+    if v_from_gpu is None:
+        a = ref.laplace2d(grid, grid)
+        b = ref.spmv(a, np.ones(n))
+        mpk = lambda start: ref.mpk(a, start, s)
+    else:
+        b, mpk = v_from_gpu
+    v1 = b / np.linalg.norm(b)
+    secs, byts = 0.0, 0.0
+    for j in range(blocks):
+        start = v1 if j == 0 else st.column(st.info().filled - 1)
+        blk = mpk(start)
+        c0 = 0 if j == 0 else st.info().filled - 1
+        t = time.perf_counter()
+        st.preprocess_block(blk, j != 0)
+        secs += time.perf_counter() - t
+        byts += 8.0 * n * (2 * c0 + 3 * (s + 1))
+    desc = (f"CPU reference BasisStore::preprocess_block (first-stage BCGS-PIP), blocks 0..{blocks - 1} "
+            f"of a restart cycle at {grid}x{grid} (n={n}), KRYLOV_NUM_THREADS={threads}")
+    return byts / secs / 1e9, secs, byts, desc
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    threads = os.cpu_count() or 1
+    K, W = args.steps, args.warmup
+    # One step = one first-stage BCGS-PIP of the reference at the bench config
+    # (a full CPU restart cycle at 4000² takes minutes).
+    import numpy as np
+    from oracle import ref
+    os.environ["KRYLOV_NUM_THREADS"] = str(threads)
+    g = args.grid
+    n = g * g
+    a = ref.laplace2d(g, g)
+    b = ref.spmv(a, np.ones(n))
+    st = ref.Store(n, 60, 5, args.shat)
+    v1 = b / np.linalg.norm(b)
+    times, byts = [], []
+    for k in range(W + K):
+        info = st.info()
+        if info.filled + 5 > 61:
+            st.reset()
+            info = st.info()
+        start = v1 if info.filled == 0 else st.column(info.filled - 1)
+        blk = ref.mpk(a, start, 5)
+        c0 = 0 if info.filled == 0 else info.filled - 1
+        t = time.perf_counter()
+        st.preprocess_block(blk, info.filled != 0)
+        dt = time.perf_counter() - t
+        if k >= W:
+            times.append(dt)
+            byts.append(8.0 * n * (2 * c0 + 18))
+    total = sum(times)
+    value = sum(byts) / total / 1e9
+    line = {
+        "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
+        "steps": K, "warmup": W, "ms_per_step": 1e3 * total / K, "higher_is_better": True, "scaling": "weak",
+        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"2D Laplace 5-pt {g}x{g}, s-step GMRES(60) s=5, two-stage BlkOrtho shat={args.shat}",
+                   "grid": [g, g], "rows": n, "step": "one first-stage BCGS-PIP (BasisStore::preprocess_block)"},
+        "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "reference",
+                         "sample": f"{K} first-stage BCGS-PIP blocks at {g}x{g} (after {W} warm-up blocks)"},
+        "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
+    }
+    print(json.dumps(line), flush=True)
+    return 0
+
+
+# ---------------------------------------------------------------------------------------
+def run_ours(args):
+    import numpy as np
+    import torch
+    import torch.distributed as dist
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    if world != args.gpus and world > 1:
+        raise SystemExit(f"--gpus {args.gpus} but WORLD_SIZE={world}")
+    torch.cuda.set_device(local)
+    import paper_2402_15033_b200 as kb
+
+    nccl_id = None
+    if world > 1:
+        dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+        idb = torch.zeros(kb.lib().kry_nccl_unique_id_size(), dtype=torch.uint8, device="cuda")
+        if rank == 0:
+            idb.copy_(torch.frombuffer(bytearray(kb.Context.nccl_unique_id()), dtype=torch.uint8))
+        dist.broadcast(idb, 0)
+        nccl_id = bytes(idb.cpu().tolist())
+    ctx = kb.Context(local, world, rank, nccl_id)
+    ctx.set_timing(True)
+    stream = torch.cuda.ExternalStream(ctx.stream_handle())
+
+    g = args.grid
+    nx, ny = g, g * world
+    op = kb.Laplace2D(nx, ny, ctx)
+    n = op.n
+    kind = kb.OrthoKind.TWO_STAGE if args.scheme == "two-stage" else kb.OrthoKind.BCGS_PIP2
+    cfg_cycle = kb.SolverConfig(scheme=kb.OrthoScheme(kind, args.shat), big_step=args.shat if kind == 3 else 0,
+                                max_iters=60)
+    ones = torch.ones(n, dtype=torch.float64, device="cuda")
+    b = torch.empty(n, dtype=torch.float64, device="cuda")
+    x = torch.zeros(n, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()
+    kb.lib().kry_spmv_device(ctx.handle, op.handle, ones.data_ptr(), b.data_ptr())  # b = A·1 (gen_rhs_ones)
+
+    def barrier():
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+
+    def cycle():
+        return kb.sstep_gmres_device(op, b.data_ptr(), x.data_ptr(), cfg_cycle, x.data_ptr())
+
+    for _ in range(args.warmup):
+        cycle()
+    barrier()
+    tel = {k: 0.0 for k in ("ortho_seconds", "ortho_bytes", "gram_kernel_seconds", "gram_bytes", "gram_launches",
+                            "update_kernel_seconds", "update_bytes", "update_launches", "mpk_seconds", "mpk_bytes",
+                            "restart_seconds", "gpu_launches")}
+    iters, reduces = 0, 0
+    ev0, ev1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    with Clocks(local) as clk:
+        ev0.record(stream)
+        for _ in range(args.steps):
+            rep = cycle()
+            for k in tel:
+                tel[k] += rep.telemetry[k]
+            iters += rep.iterations
+            reduces += rep.sync.reduces
+        ev1.record(stream)
+        ev1.synchronize()
+    barrier()
+    elapsed = ev0.elapsed_time(ev1) * 1e-3
+
+    # max over ranks of the times, sum over ranks of the bytes
+    def allred(vals, op_):
+        t = torch.tensor(vals, dtype=torch.float64, device="cuda")
+        if world > 1:
+            dist.all_reduce(t, op=op_)
+        return t.cpu().tolist()
+
+    MAX = dist.ReduceOp.MAX if world > 1 else None
+    SUM = dist.ReduceOp.SUM if world > 1 else None
+    t_el, t_ortho, t_gram, t_upd, t_mpk, t_rst = allred(
+        [elapsed, tel["ortho_seconds"], tel["gram_kernel_seconds"], tel["update_kernel_seconds"],
+         tel["mpk_seconds"], tel["restart_seconds"]], MAX)
+    b_ortho, b_gram, b_upd, b_mpk = allred([tel["ortho_bytes"], tel["gram_bytes"], tel["update_bytes"],
+                                            tel["mpk_bytes"]], SUM)
+    value = b_ortho / t_ortho / 1e9
+
+    # e2e: the host-buffer C ABI, copies inside the timed region
+    e2e = None
+    if not args.no_e2e:
+        hb = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        hb.copy_(b)
+        hx = torch.empty(n, dtype=torch.float64, pin_memory=True)
+        hx.copy_(x)
+        import ctypes as C
+        P = lambda t: C.cast(C.c_void_p(t.data_ptr()), kb._capi.P_dbl)
+        ccfg = cfg_cycle.to_c()
+        e_bytes = 0.0
+        barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            rep_c, cyc, pb, pbp = kb._new_report(1024)
+            kb._check(kb.lib().kry_sstep_gmres(ctx.handle, op.handle, P(hb), P(hx), C.byref(ccfg), C.byref(rep_c),
+                                               P(hx)))
+            e_bytes += rep_c.ortho_bytes
+        barrier()
+        t_e2e = allred([time.perf_counter() - t0], MAX)[0]
+        e_bytes = allred([e_bytes], SUM)[0]
+        e2e = {"value": e_bytes / t_e2e / 1e9, "unit": "GB/s", "h2d_bytes_per_step": 2 * 8 * n,
+               "d2h_bytes_per_step": 8 * n,
+               "definition": "BlkOrtho algorithmic bytes / end-to-end wall time of whole restart cycles via "
+                             "kry_sstep_gmres with host (pinned) b, x0 in and x out per step"}
+
+    # roofline: the dominant BlkOrtho kernel, per-launch average of this rank
+    peak, peak_src = peaks()
+    dom = "gram_kernel" if t_gram >= t_upd else "update_kernel"
+    if dom == "gram_kernel":
+        per_launch_b = tel["gram_bytes"] / max(tel["gram_launches"], 1)
+        per_launch_t = tel["gram_kernel_seconds"] / max(tel["gram_launches"], 1)
+    else:
+        per_launch_b = tel["update_bytes"] / max(tel["update_launches"], 1)
+        per_launch_t = tel["update_kernel_seconds"] / max(tel["update_launches"], 1)
+    achieved = per_launch_b / per_launch_t / 1e9
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        try:
+            with open(tpath) as f:
+                tj = json.load(f)
+            key = f"{dom}@{nx}x{g}"
+            traffic = tj.get(key)
+        except Exception:
+            traffic = None
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        def gpu_mpk(start):
+            return op.mpk(start, 5)
+        bh = b.cpu().numpy()
+        gbs, secs, byts, desc = reference_blkortho_sample(g, args.shat, args.cpu_sample_blocks, 1,
+                                                          v_from_gpu=(bh, gpu_mpk))
+        cpu = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "reference",
+               "sample": desc + f"; {secs:.1f} s of CPU BlkOrtho ({byts / 1e9:.1f} GB algorithmic); V blocks "
+                                "from the bit-identical GPU MPK"}
+
+    tts = None
+    if args.tts and world == 1:
+        x.zero_()
+        cfg_full = kb.SolverConfig(scheme=kb.OrthoScheme(kind, args.shat), big_step=args.shat if kind == 3 else 0)
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        rep = kb.sstep_gmres_device(op, b.data_ptr(), None, cfg_full, x.data_ptr())
+        tts = {"seconds": time.perf_counter() - t0, "status": rep.status.name.lower(), "iterations": rep.iterations,
+               "restarts": rep.restarts, "final_relative_residual": rep.final_relative_residual,
+               "reduces": rep.sync.reduces}
+
+    if rank == 0:
+        steps = args.steps
+        line = {
+            "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_el / steps, "higher_is_better": True, "scaling": "weak",
+            "vs_baseline": None, "dtype": "f64", "data": "synthetic (b = A*1, x0 = 0, then warm restarts)",
+            "config": {"workload": f"2D Laplace 5-pt {nx}x{ny} ({g}x{g} rows per GPU), s-step GMRES(60) s=5, "
+                                   f"{args.scheme} BlkOrtho shat={args.shat}",
+                       "grid": [nx, ny], "rows_per_gpu": n, "m": 60, "s": 5, "shat": args.shat,
+                       "step": "one full restart cycle (60 iterations) through kry_sstep_gmres_device",
+                       "parallelism": f"row-partitioned dp{world}", "l2": "inputs larger than L2 (basis 8*61*n B)"},
+            "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
+                         "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,
+                         "algorithmic_bytes_per_launch": per_launch_b, "avg_launch_ms": per_launch_t * 1e3},
+            "cpu_baseline": cpu,
+            "e2e": e2e,
+            "gpu_launches": int(tel["gpu_launches"]),
+            "clocks": clk.summary(),
+            "phases_ms_per_step": {"mpk": 1e3 * t_mpk / steps, "blkortho": 1e3 * t_ortho / steps,
+                                   "gram_kernels": 1e3 * t_gram / steps, "update_kernels": 1e3 * t_upd / steps,
+                                   "restart": 1e3 * t_rst / steps},
+            "phase_gbs": {"gram": b_gram / t_gram / 1e9, "update": b_upd / t_upd / 1e9,
+                          "mpk": b_mpk / max(t_mpk, 1e-12) / 1e9},
+            "iterations_per_step": iters / steps, "reduces_per_step": reduces / steps,
+        }
+        if tts is not None:
+            line["time_to_solution"] = tts
+        print(json.dumps(line), flush=True)
+    del op
+    ctx.close()
+    if world > 1:
+        dist.destroy_process_group()
+    return 0
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        return run_reference(args)
+    return run_ours(args)
+
+
+if __name__ == "__main__":
+    sys.exit(main())

@@ -148,6 +148,8 @@ int kry_ctx_synchronize(kry_ctx* ctx);
 int kry_ctx_set_timing(kry_ctx* ctx, int enabled);
 int kry_ctx_launch_count(kry_ctx* ctx, int64_t* launches);
 int kry_ctx_rank(kry_ctx* ctx, int* rank, int* nranks);
+/* The cudaStream_t every kernel of this context is launched on (for event timing). */
+int kry_ctx_stream(kry_ctx* ctx, void** stream);
 
 /* ---- operators (krylov::CsrMatrix csr_matrix.hpp:17-65, spmv :69-79) ----- */
 typedef struct kry_operator kry_operator;

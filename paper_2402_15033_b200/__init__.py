@@ -266,6 +266,12 @@ class Context:
     def synchronize(self) -> None:
         _check(lib().kry_ctx_synchronize(self._h))
 
+    def stream_handle(self) -> int:
+        """cudaStream_t (as an integer) all kernels of this context run on."""
+        v = C.c_void_p()
+        _check(lib().kry_ctx_stream(self._h, C.byref(v)))
+        return v.value or 0
+
     def launch_count(self) -> int:
         v = C.c_int64()
         _check(lib().kry_ctx_launch_count(self._h, C.byref(v)))

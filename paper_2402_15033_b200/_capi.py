@@ -80,6 +80,7 @@ SIGNATURES = {
     "kry_ctx_set_timing": (C.c_int, [vp, C.c_int]),
     "kry_ctx_launch_count": (C.c_int, [vp, P_i64]),
     "kry_ctx_rank": (C.c_int, [vp, C.POINTER(C.c_int), C.POINTER(C.c_int)]),
+    "kry_ctx_stream": (C.c_int, [vp, C.POINTER(vp)]),
     "kry_operator_create_csr": (C.c_int, [vp, i64, i64, i64, P_i64, P_i64, P_dbl, C.POINTER(vp)]),
     "kry_operator_create_laplace2d": (C.c_int, [vp, i64, i64, C.POINTER(vp)]),
     "kry_operator_create_laplace3d": (C.c_int, [vp, i64, i64, i64, C.POINTER(vp)]),

@@ -55,6 +55,14 @@ __device__ __forceinline__ double acc_term(double s, double coeff, double x) {
     return __dadd_rn(s, __dmul_rn(coeff, x));
 }
 
+constexpr int kLinesPerThread = 8;
+
+// x over one grid line (ix), y over chunks of kLinesPerThread owned lines
+// that each thread walks in order.  The 2-D kernel carries the line below
+// and the current line in registers, so each row loads one new line value
+// plus its two (L1-resident) horizontal neighbours.  All geometry is
+// precomputed on the host (no device integer division).  Ranks own whole
+// lines (2D) / planes (3D); out-of-rank neighbours come from the halos.
 template <int DIMS, bool RESID>
 __global__ void __launch_bounds__(kBlock) stencil_kernel(const StencilGeom g, const double* __restrict__ x,
                                                          const double* __restrict__ halo_lo,
@@ -62,43 +70,68 @@ __global__ void __launch_bounds__(kBlock) stencil_kernel(const StencilGeom g, co
                                                          const double* __restrict__ b,
                                                          double* __restrict__ y,
                                                          double* __restrict__ partials) {
-    // 2-D launch: x over the grid line (ix), y over this rank's grid lines
-    // (grid-stride) — no per-row integer division.  Ranks own whole lines
-    // (2D) / planes (3D); out-of-rank neighbours come from the halo planes.
-    const i64 ix = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
-    const i64 plane = g.nx * g.ny;
-    const i64 lines = g.nloc / g.nx;
-    const i64 line0 = g.row_begin / g.nx;
-    const i64 z0 = g.row_begin / plane, nzl = g.nloc / plane;
+    const i64 ix = blockIdx.x * static_cast<i64>(kBlock) + threadIdx.x;
+    const i64 nx = g.nx;
     double sq = 0.0;
-    for (i64 L = blockIdx.y; L < lines; L += gridDim.y) {
-        if (ix >= g.nx) continue;
-        const i64 i = L * g.nx + ix;  // local row
-        const i64 gl = line0 + L;     // global grid line
-        double s = 0.0;
-        if (DIMS == 2) {
-            if (gl > 0) s = acc_term(s, -1.0, L > 0 ? x[i - g.nx] : halo_lo[ix]);
-            if (ix > 0) s = acc_term(s, -1.0, x[i - 1]);
-            s = acc_term(s, 4.0, x[i]);
-            if (ix + 1 < g.nx) s = acc_term(s, -1.0, x[i + 1]);
-            if (gl + 1 < g.ny) s = acc_term(s, -1.0, L + 1 < lines ? x[i + g.nx] : halo_hi[ix]);
-        } else {
-            const i64 iz = gl / g.ny, iy = gl - iz * g.ny, zl = iz - z0;
-            const i64 hp = iy * g.nx + ix;  // offset inside a halo plane
-            if (iz > 0) s = acc_term(s, -1.0, zl > 0 ? x[i - plane] : halo_lo[hp]);
-            if (iy > 0) s = acc_term(s, -1.0, x[i - g.nx]);
-            if (ix > 0) s = acc_term(s, -1.0, x[i - 1]);
-            s = acc_term(s, 6.0, x[i]);
-            if (ix + 1 < g.nx) s = acc_term(s, -1.0, x[i + 1]);
-            if (iy + 1 < g.ny) s = acc_term(s, -1.0, x[i + g.nx]);
-            if (iz + 1 < g.nz) s = acc_term(s, -1.0, zl + 1 < nzl ? x[i + plane] : halo_hi[hp]);
-        }
-        if (RESID) {
-            const double r = __dsub_rn(b[i], s);
-            y[i] = r;
-            sq = fma(r, r, sq);
-        } else {
-            y[i] = s;
+    if (ix < nx) {
+        for (i64 lc = static_cast<i64>(blockIdx.y) * kLinesPerThread; lc < g.lines;
+             lc += static_cast<i64>(gridDim.y) * kLinesPerThread) {
+            const i64 lend = min(lc + kLinesPerThread, g.lines);
+            i64 i = lc * nx + ix;  // local row
+            if (DIMS == 2) {
+                i64 gl = g.line0 + lc;  // global grid line
+                double down = 0.0;
+                if (gl > 0) down = lc > 0 ? x[i - nx] : halo_lo[ix];
+                double cur = x[i];
+                for (i64 l = lc; l < lend; ++l, ++gl, i += nx) {
+                    const bool has_up = gl + 1 < g.ny;
+                    double up = 0.0;
+                    if (has_up) up = l + 1 < g.lines ? x[i + nx] : halo_hi[ix];
+                    double s = 0.0;
+                    if (gl > 0) s = acc_term(s, -1.0, down);
+                    if (ix > 0) s = acc_term(s, -1.0, x[i - 1]);
+                    s = acc_term(s, 4.0, cur);
+                    if (ix + 1 < nx) s = acc_term(s, -1.0, x[i + 1]);
+                    if (has_up) s = acc_term(s, -1.0, up);
+                    if (RESID) {
+                        const double r = __dsub_rn(b[i], s);
+                        y[i] = r;
+                        sq = fma(r, r, sq);
+                    } else {
+                        y[i] = s;
+                    }
+                    down = cur;
+                    cur = up;
+                }
+            } else {
+                const i64 plane = nx * g.ny;
+                const i64 gl0 = g.line0 + lc;
+                i64 iz = gl0 / g.ny;  // once per chunk
+                i64 iy = gl0 - iz * g.ny;
+                for (i64 l = lc; l < lend; ++l, i += nx) {
+                    const i64 zl = iz - g.z0;
+                    const i64 hp = iy * nx + ix;  // offset inside a halo plane
+                    double s = 0.0;
+                    if (iz > 0) s = acc_term(s, -1.0, zl > 0 ? x[i - plane] : halo_lo[hp]);
+                    if (iy > 0) s = acc_term(s, -1.0, x[i - nx]);
+                    if (ix > 0) s = acc_term(s, -1.0, x[i - 1]);
+                    s = acc_term(s, 6.0, x[i]);
+                    if (ix + 1 < nx) s = acc_term(s, -1.0, x[i + 1]);
+                    if (iy + 1 < g.ny) s = acc_term(s, -1.0, x[i + nx]);
+                    if (iz + 1 < g.nz) s = acc_term(s, -1.0, zl + 1 < g.nzl ? x[i + plane] : halo_hi[hp]);
+                    if (RESID) {
+                        const double r = __dsub_rn(b[i], s);
+                        y[i] = r;
+                        sq = fma(r, r, sq);
+                    } else {
+                        y[i] = s;
+                    }
+                    if (++iy == g.ny) {
+                        iy = 0;
+                        ++iz;
+                    }
+                }
+            }
         }
     }
     if (RESID) {
@@ -177,8 +210,24 @@ int grid_for(i64 n) {
 int reduce_grid() { return num_sms() * 16; }
 
 dim3 stencil_grid(const StencilGeom& g) {
-    const i64 lines = std::max<i64>(1, g.nloc / g.nx);
-    return dim3(static_cast<unsigned>(ceil_div(g.nx, kBlock)), static_cast<unsigned>(std::min<i64>(lines, 65535)));
+    const i64 chunks = std::max<i64>(1, ceil_div(g.lines, kLinesPerThread));
+    return dim3(static_cast<unsigned>(ceil_div(g.nx, kBlock)), static_cast<unsigned>(std::min<i64>(chunks, 65535)));
+}
+
+StencilGeom make_stencil_geom(int dims, i64 nx, i64 ny, i64 nz, i64 row_begin, i64 nloc) {
+    StencilGeom g{};
+    g.dims = dims;
+    g.nx = nx;
+    g.ny = ny;
+    g.nz = dims == 2 ? 1 : nz;
+    g.row_begin = row_begin;
+    g.nloc = nloc;
+    g.halo = dims == 2 ? nx : nx * ny;
+    g.lines = nloc / nx;
+    g.line0 = row_begin / nx;
+    g.z0 = dims == 2 ? 0 : row_begin / (nx * ny);
+    g.nzl = dims == 2 ? 0 : nloc / (nx * ny);
+    return g;
 }
 
 int stencil_partials(const StencilGeom& g) {

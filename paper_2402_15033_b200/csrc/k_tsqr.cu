@@ -30,6 +30,7 @@
 #include <algorithm>
 #include <cstring>
 #include <mutex>
+#include <unordered_map>
 #include <vector>
 
 #include "kb_common.hpp"
@@ -39,8 +40,9 @@ namespace kb {
 
 namespace {
 
-constexpr int kConsumerWarps = 4;
-constexpr int kThreads = (kConsumerWarps + 1) * 32;  // + producer warp
+// Consumer warps per CTA: 8 while the accumulators are small, 4 for the
+// widest Gram shapes (≥ 30 register-resident tiles) to stay spill-free.
+__host__ __device__ constexpr int consumer_warps(int nbw) { return nbw >= 5 ? 4 : 8; }
 constexpr int kSmemBudget = 200 * 1024;
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {
@@ -90,6 +92,7 @@ struct TsParams {
     int cpslots;    // round_up(cp, 8)
     int stages;
     int vv;         // gram: compute the VᵀV tiles in this pass
+    int consumers;  // consumer warps (empty-barrier arrival count)
     int first;      // update: V holds the raw block (else the running partial)
     int last;       // update: apply the triangular solve and the scaling
     unsigned tx_bytes;
@@ -106,7 +109,7 @@ __device__ __forceinline__ double* ring_setup(unsigned char* smem, const TsParam
     if (threadIdx.x == 0) {
         for (int s = 0; s < p.stages; ++s) {
             mbar_init(&full[s], 1);
-            mbar_init(&empty[s], kConsumerWarps);
+            mbar_init(&empty[s], p.consumers);
         }
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
@@ -127,122 +130,156 @@ __device__ __forceinline__ double* ring_setup(unsigned char* smem, const TsParam
     return ring;
 }
 
-// Producer loop (one elected lane of the last warp).
+// Producer loop (one elected lane of the producer warp).  Stage index and
+// use count advance incrementally (no integer division per tile).
 __device__ __forceinline__ void ring_produce(const CUtensorMap* map_v, const CUtensorMap* map_p,
                                             const TsParams& p, double* ring, uint64_t* full,
                                             uint64_t* empty) {
     const size_t stage_doubles = static_cast<size_t>(p.wslots + p.cpslots) * p.tr;
-    int it = 0;
-    for (i64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
-        const int s = it % p.stages;
-        if (it >= p.stages) mbar_wait(&empty[s], ((it / p.stages) - 1) & 1);
+    int s = 0, use = 0;
+    for (i64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        if (use > 0) mbar_wait(&empty[s], (use - 1) & 1);
         double* st = ring + s * stage_doubles;
         mbar_expect_tx(&full[s], p.tx_bytes);
         const int row0 = static_cast<int>(tile * p.tr);
         tma_load_2d(st, map_v, row0, 0, &full[s]);
         if (p.cp > 0) tma_load_2d(st + static_cast<size_t>(p.wslots) * p.tr, map_p, row0, 0, &full[s]);
+        if (++s == p.stages) {
+            s = 0;
+            ++use;
+        }
     }
 }
 
+// Tiles of the Gram, in (jb, ib) order: jb < NBW indexes the V column blocks
+// (output columns), ib < NB the [V | P] column blocks (output rows); the
+// VᵀV part keeps only ib ≤ jb (gram() computes the upper triangle).
+__host__ __device__ constexpr bool tile_valid(int nbw, int jb, int ib) { return ib >= nbw || ib <= jb; }
+__host__ __device__ constexpr int tile_pos(int nbw, int nb, int jb, int ib) {
+    int t = 0;
+    for (int j = 0; j < nbw; ++j)
+        for (int i = 0; i < nb; ++i) {
+            if (!tile_valid(nbw, j, i)) continue;
+            if (j == jb && i == ib) return t;
+            ++t;
+        }
+    return -1;
+}
+__host__ __device__ constexpr int tile_count(int nbw, int nb) {
+    int t = 0;
+    for (int j = 0; j < nbw; ++j)
+        for (int i = 0; i < nb; ++i) t += tile_valid(nbw, j, i) ? 1 : 0;
+    return t;
+}
+
 // ---------------------------------------------------------------------------
-// K3: fused Gram  G = [V | P]ᵀ V  on DMMA.
-//   Column blocks (8 columns each): b < NBW are V blocks, NBW ≤ b < NBW+nbp
-//   are P blocks.  Tile (ib, jb), jb < NBW, is computed when ib is a P block,
-//   or a V block with ib ≤ jb (upper triangle of VᵀV) and vv is set.
+// K3: fused Gram  G = [V | P]ᵀ V  on DMMA (mma.m8n8k4.f64).
+//   Blocks of 8 columns: b < NBW are V blocks, NBW ≤ b < NB are P blocks.
+//   Rows are the MMA k dimension: each 4-row chunk contributes one DMMA per
+//   tile; a lane's fragment for block b is X[r0 + lane%4][8b + lane/4]
+//   for both operands, so one LDS per block feeds every tile of the block.
+//   The smem column stride tr ≡ 4 (mod 16) makes those loads conflict-free.
 // ---------------------------------------------------------------------------
-template <int NBW>
-__global__ void __launch_bounds__(kThreads, 1)
+template <int NBW, int NB, int CW = consumer_warps(NBW)>
+__global__ void __launch_bounds__((CW + 1) * 32, 1)
     gram_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_p,
                 const TsParams p, double* __restrict__ partials) {
+    constexpr int T = tile_count(NBW, NB);
     extern __shared__ __align__(1024) unsigned char smem[];
     uint64_t *full, *empty;
     double* ring = ring_setup(smem, p, full, empty);
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-    const int nbp = p.cpslots / 8;
     const size_t stage_doubles = static_cast<size_t>(p.wslots + p.cpslots) * p.tr;
 
-    if (warp == kConsumerWarps) {
+    if (warp == CW) {
         if (lane == 0) ring_produce(&map_v, &map_p, p, ring, full, empty);
         return;
     }
 
-    double acc[NBW][8][2];
+    double acc[NBW][NB][2];
 #pragma unroll
     for (int jb = 0; jb < NBW; ++jb)
 #pragma unroll
-        for (int ib = 0; ib < 8; ++ib) acc[jb][ib][0] = acc[jb][ib][1] = 0.0;
+        for (int ib = 0; ib < NB; ++ib) acc[jb][ib][0] = acc[jb][ib][1] = 0.0;
 
     const int frag_off = (lane >> 2) * p.tr + (lane & 3);
     const int nchunks = p.tr / 4;
-    int it = 0;
-    for (i64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x, ++it) {
-        const int s = it % p.stages;
-        mbar_wait(&full[s], (it / p.stages) & 1);
-        const double* st = ring + s * stage_doubles;
-        for (int c = (warp + it) & 3; c < nchunks; c += kConsumerWarps) {
-            const double* base = st + frag_off + 4 * c;
-            double f[8];
+    const bool vv = p.vv != 0;
+    int s = 0, use = 0, rot = warp;
+    for (i64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        mbar_wait(&full[s], use & 1);
+        const double* st = ring + s * stage_doubles + frag_off;
+#pragma unroll 2
+        for (int c = rot; c < nchunks; c += CW) {
+            const double* base = st + 4 * c;
+            double f[NB];
 #pragma unroll
-            for (int b = 0; b < 8; ++b)
-                f[b] = (b < NBW + nbp) ? base[static_cast<size_t>(8 * b) * p.tr] : 0.0;
+            for (int b = 0; b < NB; ++b) f[b] = base[static_cast<size_t>(8 * b) * p.tr];
 #pragma unroll
-            for (int jb = 0; jb < NBW; ++jb) {
+            for (int jb = 0; jb < NBW; ++jb)
 #pragma unroll
-                for (int ib = 0; ib < 8; ++ib) {
-                    if (ib < NBW) {
-                        if (ib <= jb && p.vv) dmma(acc[jb][ib][0], acc[jb][ib][1], f[ib], f[jb]);
-                    } else if (ib - NBW < nbp) {
-                        dmma(acc[jb][ib][0], acc[jb][ib][1], f[ib], f[jb]);
-                    }
+                for (int ib = 0; ib < NB; ++ib) {
+                    if (!tile_valid(NBW, jb, ib)) continue;
+                    if (ib >= NBW || vv) dmma(acc[jb][ib][0], acc[jb][ib][1], f[ib], f[jb]);
                 }
-            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
+        rot = (rot + 1) & (CW - 1);
+        if (++s == p.stages) {
+            s = 0;
+            ++use;
+        }
     }
 
     // Cross-warp reduction in fixed warp order, through the (now idle) ring.
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
-    double* scratch = ring;  // [warp][NBW*8][64]
+    asm volatile("bar.sync 1, %0;" ::"n"(CW * 32));
+    double* scratch = ring;  // [warp][T][64]
     const int e0 = (lane >> 2) + 8 * (2 * (lane & 3));
 #pragma unroll
     for (int jb = 0; jb < NBW; ++jb)
 #pragma unroll
-        for (int ib = 0; ib < 8; ++ib) {
-            double* t = scratch + (static_cast<size_t>(warp) * NBW * 8 + jb * 8 + ib) * 64;
+        for (int ib = 0; ib < NB; ++ib) {
+            if (!tile_valid(NBW, jb, ib)) continue;
+            double* t = scratch + (static_cast<size_t>(warp) * T + tile_pos(NBW, NB, jb, ib)) * 64;
             t[e0] = acc[jb][ib][0];
             t[e0 + 8] = acc[jb][ib][1];
         }
-    asm volatile("bar.sync 1, %0;" ::"n"(kConsumerWarps * 32));
-    const int per_warp = NBW * 8 * 64;
-    double* out = partials + static_cast<size_t>(blockIdx.x) * per_warp;
-    for (int e = threadIdx.x; e < per_warp; e += kConsumerWarps * 32) {
+    asm volatile("bar.sync 1, %0;" ::"n"(CW * 32));
+    constexpr int per_cta = T * 64;
+    double* out = partials + static_cast<size_t>(blockIdx.x) * per_cta;
+    for (int e = threadIdx.x; e < per_cta; e += CW * 32) {
         double sum = scratch[e];
 #pragma unroll
-        for (int w = 1; w < kConsumerWarps; ++w) sum += scratch[static_cast<size_t>(w) * per_warp + e];
+        for (int w = 1; w < CW; ++w) sum += scratch[static_cast<size_t>(w) * per_cta + e];
         out[e] = sum;
     }
 }
 
-struct TileList {
-    int count;
-    int id[64];  // jb * 8 + ib
-};
-
 // One warp per output entry: lanes sum the per-CTA partials with a fixed
 // stride, then a fixed xor tree.  Deterministic for a given grid size.
 __global__ void gram_reduce_kernel(const double* __restrict__ partials, int grid, int per_cta,
-                                   const TileList tiles, double* __restrict__ packed) {
+                                   double* __restrict__ packed) {
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
-    if (gw >= tiles.count * 64) return;
-    const int t = gw >> 6, e = gw & 63;
-    const size_t off = static_cast<size_t>(tiles.id[t]) * 64 + e;
+    if (gw >= per_cta) return;
     double s = 0.0;
-    for (int c = lane; c < grid; c += 32) s += partials[static_cast<size_t>(c) * per_cta + off];
+    for (int c = lane; c < grid; c += 32) s += partials[static_cast<size_t>(c) * per_cta + gw];
 #pragma unroll
     for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
     if (lane == 0) packed[gw] = s;
+}
+
+template <int NBW, int NB>
+const void* gram_fn(int nbw, int nb) {
+    if (nbw == NBW && nb == NB) return reinterpret_cast<const void*>(gram_kernel<NBW, NB>);
+    if constexpr (NB < 8) {
+        return gram_fn<NBW, NB + 1>(nbw, nb);
+    } else if constexpr (NBW < 8) {
+        return gram_fn<NBW + 1, NBW + 1>(nbw, nb);
+    } else {
+        return nullptr;
+    }
 }
 
 // ---------------------------------------------------------------------------
@@ -259,6 +296,8 @@ template <int WMAX>
 __global__ void __launch_bounds__(256)
     update_kernel(i64 n, const double* __restrict__ P, i64 ldp, int cp, const double* V, i64 ldv, int w,
                   const double* __restrict__ coef, int triangular, double* out, i64 ldo) {
+    // Columns w ≤ j < WMAX are identity padding (zero coefficients, inv = 1):
+    // the arithmetic below is branch-free and leaves them at zero.
     extern __shared__ __align__(16) double c_sm[];
     const int ncoef = (cp + WMAX + 1) * WMAX;
     for (int i = threadIdx.x; i < ncoef; i += blockDim.x) c_sm[i] = coef[i];
@@ -279,27 +318,40 @@ __global__ void __launch_bounds__(256)
             for (int u = 0; u < 4; ++u) pv[u] = __ldg(prow + (l + u) * ldp);
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const double* cr = nrc + (l + u) * WMAX;
+                const double2* cr = reinterpret_cast<const double2*>(nrc + (l + u) * WMAX);
 #pragma unroll
-                for (int j = 0; j < WMAX; ++j)
-                    if (j < w) acc[j] = fma(cr[j], pv[u], acc[j]);
+                for (int j = 0; j < WMAX; j += 2) {
+                    const double2 c = cr[j / 2];
+                    acc[j] = fma(c.x, pv[u], acc[j]);
+                    acc[j + 1] = fma(c.y, pv[u], acc[j + 1]);
+                }
             }
         }
         for (; l < cp; ++l) {
             const double pv = __ldg(prow + l * ldp);
-            const double* cr = nrc + l * WMAX;
+            const double2* cr = reinterpret_cast<const double2*>(nrc + l * WMAX);
 #pragma unroll
-            for (int j = 0; j < WMAX; ++j)
-                if (j < w) acc[j] = fma(cr[j], pv, acc[j]);
+            for (int j = 0; j < WMAX; j += 2) {
+                const double2 c = cr[j / 2];
+                acc[j] = fma(c.x, pv, acc[j]);
+                acc[j + 1] = fma(c.y, pv, acc[j + 1]);
+            }
         }
         if (triangular) {
+            // Right-looking substitution: acc_j receives −R(k,j)·x_k for
+            // k = 0, 1, … in order, then ×1/R(j,j) — tri_solve_right's order.
 #pragma unroll
             for (int k = 0; k < WMAX; ++k) {
-                if (k < w) {
-                    acc[k] *= inv[k];
+                acc[k] *= inv[k];
+                const double* rk = nrjj + k * WMAX;
+                if ((k + 1) & 1) {  // odd first column: one scalar step to reach a pair boundary
+                    if (k + 1 < WMAX) acc[k + 1] = fma(rk[k + 1], acc[k], acc[k + 1]);
+                }
 #pragma unroll
-                    for (int j = k + 1; j < WMAX; ++j)
-                        if (j < w) acc[j] = fma(nrjj[k * WMAX + j], acc[k], acc[j]);
+                for (int j = (k + 2) & ~1; j < WMAX; j += 2) {
+                    const double2 c = *reinterpret_cast<const double2*>(rk + j);
+                    acc[j] = fma(c.x, acc[k], acc[j]);
+                    acc[j + 1] = fma(c.y, acc[k], acc[j + 1]);
                 }
             }
         }
@@ -309,6 +361,74 @@ __global__ void __launch_bounds__(256)
     }
 }
 
+// Wide blocks (33 ≤ w ≤ 64, the ŝ+1 finalize panel): two threads per row.
+// Thread parity p owns columns j ≡ p (mod 2); each finalized x_k is passed
+// to the partner with one shuffle.  Half the accumulators per thread → twice
+// the resident warps, which the 64-step substitution chain needs.
+// coef layout: nrc[cp][2][32] and nrjj[64][2][32] (column j = 2·jj + parity),
+// inv[2][32].
+__global__ void __launch_bounds__(256)
+    update_pair_kernel(i64 n, const double* __restrict__ P, i64 ldp, int cp, const double* V, i64 ldv, int w,
+                       const double* __restrict__ coef, int triangular, double* out, i64 ldo) {
+    constexpr int H = 32;
+    extern __shared__ __align__(16) double c_sm[];
+    const int ncoef = (cp + 64 + 1) * 64;
+    for (int i = threadIdx.x; i < ncoef; i += blockDim.x) c_sm[i] = coef[i];
+    __syncthreads();
+    const int par = threadIdx.x & 1;
+    const double* nrc = c_sm + par * H;
+    const double* nrjj = c_sm + static_cast<size_t>(cp) * 64 + par * H;
+    const double* inv = c_sm + static_cast<size_t>(cp + 64) * 64 + par * H;
+    const unsigned lane = threadIdx.x & 31;
+    const i64 pairs = static_cast<i64>(gridDim.x) * (blockDim.x / 2);
+    // Every thread runs the same trip count (shuffles stay convergent).
+    for (i64 base = blockIdx.x * static_cast<i64>(blockDim.x / 2); base < n; base += pairs) {
+        const i64 row = base + (threadIdx.x >> 1);
+        const bool live = row < n;
+        double acc[H];
+#pragma unroll
+        for (int jj = 0; jj < H; ++jj) {
+            const int j = 2 * jj + par;
+            acc[jj] = (live && j < w) ? V[row + j * ldv] : 0.0;
+        }
+        const double* prow = P + (live ? row : 0);
+        for (int l = 0; l < cp; ++l) {
+            const double pv = __ldg(prow + l * ldp);
+            const double2* cr = reinterpret_cast<const double2*>(nrc + l * 64);
+#pragma unroll
+            for (int jj = 0; jj < H; jj += 2) {
+                const double2 c = cr[jj / 2];
+                acc[jj] = fma(c.x, pv, acc[jj]);
+                acc[jj + 1] = fma(c.y, pv, acc[jj + 1]);
+            }
+        }
+        if (triangular) {
+#pragma unroll
+            for (int k = 0; k < 64; ++k) {
+                const int kk = k >> 1;
+                double xk = 0.0;
+                if ((k & 1) == par) {
+                    acc[kk] *= inv[kk];
+                    xk = acc[kk];
+                }
+                xk = __shfl_sync(0xffffffffu, xk, (lane & ~1u) | static_cast<unsigned>(k & 1));
+                // columns j > k owned by this thread: jj from first(j > k, j ≡ par)
+                const int first = (k + 1 + ((k + 1 + par) & 1)) >> 1;  // smallest jj with 2jj+par > k
+                const double* rk = nrjj + k * 64;
+#pragma unroll
+                for (int jj = 0; jj < H; ++jj)
+                    if (jj >= first) acc[jj] = fma(rk[jj], xk, acc[jj]);
+            }
+        }
+        if (live) {
+#pragma unroll
+            for (int jj = 0; jj < H; ++jj) {
+                const int j = 2 * jj + par;
+                if (j < w) out[row + j * ldo] = acc[jj];
+            }
+        }
+    }
+}
 
 // ---------------------------------------------------------------------------
 // Host side: tensor maps, geometry, launches.
@@ -357,10 +477,15 @@ int sm_count() {
     return n;
 }
 
-template <typename K>
-void set_smem(K kernel, size_t bytes) {
-    KB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize,
-                                 static_cast<int>(bytes)));
+// cudaFuncSetAttribute once per kernel and size (it is a host-side call per launch otherwise).
+void set_smem(const void* kernel, size_t bytes) {
+    static std::mutex mu;
+    static std::unordered_map<const void*, size_t> done;
+    std::lock_guard<std::mutex> lock(mu);
+    size_t& have = done[kernel];
+    if (bytes <= have) return;
+    KB_CUDA(cudaFuncSetAttribute(kernel, cudaFuncAttributeMaxDynamicSharedMemorySize, static_cast<int>(bytes)));
+    have = bytes;
 }
 
 TsParams geometry(i64 n, int w, int cp, bool gram) {
@@ -411,7 +536,8 @@ std::vector<std::pair<i64, i64>> prefix_groups(i64 c0, i64 w) {
 }
 
 i64 gram_scratch_doubles(i64 w) {
-    return static_cast<i64>(sm_count()) * round_up(w, 8) / 8 * 8 * 64;
+    (void)w;
+    return static_cast<i64>(sm_count()) * 36 * 64;
 }
 
 void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V,
@@ -419,44 +545,27 @@ void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 
                       std::vector<int>& tile_ids, int64_t& launches) {
     TsParams p = geometry(n, static_cast<int>(w), static_cast<int>(cp), true);
     p.vv = vv ? 1 : 0;
-    const int nbw = p.wslots / 8, nbp = p.cpslots / 8;
+    const int nbw = p.wslots / 8, nb = nbw + p.cpslots / 8;
     tile_ids.clear();
     for (int jb = 0; jb < nbw; ++jb)
-        for (int ib = 0; ib < 8; ++ib) {
-            const bool ok = (ib < nbw) ? (ib <= jb && vv) : (ib - nbw < nbp);
-            if (ok) tile_ids.push_back(jb * 8 + ib);
-        }
-    if (tile_ids.empty()) return;
+        for (int ib = 0; ib < nb; ++ib)
+            if (tile_valid(nbw, jb, ib)) tile_ids.push_back(jb * 8 + ib);
+    const int T = static_cast<int>(tile_ids.size());
     CUtensorMap mv = make_map(V, ldv, n, w, p.tr);
     CUtensorMap mp = make_map(P, ldp, n, cp, p.tr);
     const int grid = static_cast<int>(std::min<i64>(sm_count(), std::max<i64>(1, p.ntiles)));
-    const size_t red_bytes = static_cast<size_t>(kConsumerWarps) * nbw * 8 * 64 * 8;
+    const int cw = consumer_warps(nbw);
+    p.consumers = cw;
+    const size_t red_bytes = static_cast<size_t>(cw) * T * 64 * 8;
     const size_t smem = std::max(ring_bytes(p), red_bytes) + 1024;
-    switch (nbw) {
-#define KB_GRAM_CASE(NB)                                                                   \
-    case NB:                                                                               \
-        set_smem(gram_kernel<NB>, smem);                                                   \
-        gram_kernel<NB><<<grid, kThreads, smem, stream>>>(mv, mp, p, d_partials);          \
-        break;
-        KB_GRAM_CASE(1)
-        KB_GRAM_CASE(2)
-        KB_GRAM_CASE(3)
-        KB_GRAM_CASE(4)
-        KB_GRAM_CASE(5)
-        KB_GRAM_CASE(6)
-        KB_GRAM_CASE(7)
-        KB_GRAM_CASE(8)
-#undef KB_GRAM_CASE
-        default:
-            fail(KRY_UNSUPPORTED, "gram width");
-    }
+    const void* fn = gram_fn<1, 1>(nbw, nb);
+    if (!fn) fail(KRY_UNSUPPORTED, "gram shape");
+    set_smem(fn, smem);
+    void* args[] = {&mv, &mp, &p, &d_partials};
+    KB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3((cw + 1) * 32), args, smem, stream));
     KB_LAUNCHED();
-    TileList tl{};
-    tl.count = static_cast<int>(tile_ids.size());
-    for (int i = 0; i < tl.count; ++i) tl.id[i] = tile_ids[i];
-    const int warps = tl.count * 64;
-    gram_reduce_kernel<<<ceil_div(warps * 32, 256), 256, 0, stream>>>(d_partials, grid, nbw * 8 * 64,
-                                                                       tl, d_packed);
+    const int per_cta = T * 64;
+    gram_reduce_kernel<<<ceil_div(per_cta * 32, 256), 256, 0, stream>>>(d_partials, grid, per_cta, d_packed);
     KB_LAUNCHED();
     launches += 2;
 }
@@ -469,10 +578,10 @@ void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp,
     const size_t smem = static_cast<size_t>(cp + wmax + 1) * wmax * 8;
     if (smem > 200 * 1024) fail(KRY_UNSUPPORTED, "update coefficients exceed shared memory");
     auto go = [&](auto kernel) {
-        set_smem(kernel, smem);
+        set_smem(reinterpret_cast<const void*>(kernel), smem);
         int per_sm = 0;
         KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem));
-        const i64 want = ceil_div(n, 256);
+        const i64 want = ceil_div(n, wmax == 64 ? 128 : 256);
         const int grid = static_cast<int>(std::max<i64>(1, std::min<i64>(want, static_cast<i64>(sm_count()) * std::max(per_sm, 1))));
         kernel<<<grid, 256, smem, stream>>>(n, P, ldp, static_cast<int>(cp), V, ldv, static_cast<int>(w), d_coef,
                                             triangular ? 1 : 0, out, ldo);
@@ -481,7 +590,7 @@ void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp,
         case 8: go(update_kernel<8>); break;
         case 16: go(update_kernel<16>); break;
         case 32: go(update_kernel<32>); break;
-        default: go(update_kernel<64>); break;
+        default: go(update_pair_kernel); break;  // coefficients in the interleaved layout
     }
     KB_LAUNCHED();
     launches += 1;

@@ -20,6 +20,7 @@ using kb::i64;
 struct kry_ctx {
     std::unique_ptr<kb::Ctx> c;
     kb::DevBuf up0, up1, up2;  // staging for host-view entry points
+    kb::Workspace ws;          // solver workspace reused across solves (destroyed before c)
 };
 struct kry_operator {
     std::unique_ptr<kb::Operator> op;
@@ -240,9 +241,7 @@ int kry_ctx_destroy(kry_ctx* ctx) {
     return guarded([&] {
         if (!ctx) return;
         if (ctx->c) kb::bind_device(*ctx->c);
-        ctx->up0.release();
-        ctx->up1.release();
-        ctx->up2.release();
+        ctx->ws.store.reset();
         delete ctx;
     });
 }
@@ -258,6 +257,10 @@ int kry_ctx_rank(kry_ctx* ctx, int* rank, int* nranks) {
         if (rank) *rank = c.rank;
         if (nranks) *nranks = c.nranks;
     });
+}
+
+int kry_ctx_stream(kry_ctx* ctx, void** stream) {
+    return guarded([&] { *stream = static_cast<void*>(C(ctx).stream); });
 }
 
 // ---- operators -------------------------------------------------------------
@@ -700,13 +703,13 @@ static int solve_common(kry_ctx* ctx, kry_operator* op, const double* b, const d
         Snapshot snap(c);
         kb::Report rep;
         if (device) {
-            rep = kb::gmres(c, *op->op, b, x0, *cfg, standard, x_out);
+            rep = kb::gmres(c, *op->op, b, x0, *cfg, standard, x_out, &ctx->ws);
         } else {
             const i64 ld = kb::device_ld(n);
             double* db = upload(c, ctx->up0, b, n, 1);
             double* dx0 = x0 ? upload(c, ctx->up1, x0, n, 1) : nullptr;
             ctx->up2.ensure(static_cast<size_t>(ld) * 8);
-            rep = kb::gmres(c, *op->op, db, dx0, *cfg, standard, ctx->up2.p);
+            rep = kb::gmres(c, *op->op, db, dx0, *cfg, standard, ctx->up2.p, &ctx->ws);
             download(c, x_out, ctx->up2.p, ld, n, 1);
             c.sync();
         }

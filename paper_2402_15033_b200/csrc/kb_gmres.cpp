@@ -27,7 +27,7 @@ struct Vec {
 }  // namespace
 
 Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, const kry_solver_config& cfg_in,
-             bool standard_mode, double* d_x_out) {
+             bool standard_mode, double* d_x_out, Workspace* ws) {
     kry_solver_config cfg = cfg_in;
     if (standard_mode) {  // standard_gmres (gmres.hpp:404-411)
         cfg.step = 1;
@@ -45,7 +45,16 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
 
     Report rep;
     const size_t vbytes = static_cast<size_t>(device_ld(n)) * 8;
-    DevBuf x, xn, r, rn;
+    Workspace local;
+    Workspace& W = ws ? *ws : local;
+    if (W.n != n || W.m != m || W.s != s || W.shat != shat) {
+        W.store.reset();
+        W.n = n;
+        W.m = m;
+        W.s = s;
+        W.shat = shat;
+    }
+    DevBuf &x = W.x, &xn = W.xn, &r = W.r, &rn = W.rn;
     x.ensure(vbytes);
     xn.ensure(vbytes);
     r.ensure(vbytes);
@@ -81,7 +90,9 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         return rep;
     }
 
-    Store store(ctx, n, m, s, shat);
+    if (!W.store) W.store = std::make_unique<Store>(ctx, n, m, s, shat);
+    Store& store = *W.store;
+    store.ortho_bytes = 0.0;
     const int scheme = cfg.scheme_kind;
 
     auto usable_cols = [&]() -> i64 {

@@ -5,6 +5,7 @@
 // cross to the host.
 #pragma once
 
+#include <memory>
 #include <vector>
 
 #include "kb_operator.hpp"
@@ -28,9 +29,18 @@ struct Report {
     double mpk_bytes = 0.0, ortho_bytes = 0.0;
 };
 
-// d_b: n_local rhs (device); d_x0 may be null; d_x_out (n_local) may be null.
+// Device workspace of one solve (basis store + four vectors), kept by the
+// C-ABI context so that repeated solves of the same shape reuse HBM instead
+// of re-allocating (and re-zeroing) an n×(m+1) basis per call.
+struct Workspace {
+    i64 n = -1, m = -1, s = -1, shat = -1;
+    std::unique_ptr<Store> store;
+    DevBuf x, xn, r, rn;
+};
+
+// d_b: n_local rhs (device); d_x0 may be null (or alias d_x_out); d_x_out may be null.
 Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, const kry_solver_config& cfg,
-             bool standard_mode, double* d_x_out);
+             bool standard_mode, double* d_x_out, Workspace* ws = nullptr);
 
 void validate_config(const kry_solver_config& cfg);
 

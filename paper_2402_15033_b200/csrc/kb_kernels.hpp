@@ -31,7 +31,13 @@ struct StencilGeom {
     i64 row_begin;   // first global row owned
     i64 nloc;        // rows owned
     i64 halo;        // halo length (nx for 2D, nx*ny for 3D)
+    // derived on the host (kernel-uniform, no device division):
+    i64 lines;       // owned grid lines (nloc / nx)
+    i64 line0;       // global index of the first owned line
+    i64 z0;          // first owned plane (3D)
+    i64 nzl;         // owned planes (3D)
 };
+StencilGeom make_stencil_geom(int dims, i64 nx, i64 ny, i64 nz, i64 row_begin, i64 nloc);
 // y = A·x (b == nullptr) or r = b − A·x with Σr² partials (b != nullptr);
 // returns the number of partials written.
 int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const double* halo_lo,

@@ -34,7 +34,7 @@ Operator* make_laplace(Ctx& ctx, int dims, i64 nx, i64 ny, i64 nz) {
     op->row_begin = l0 * plane;
     op->nloc = (l1 - l0) * plane;
     op->nnz_local = 0;
-    op->geom = StencilGeom{dims, nx, ny, dims == 2 ? 1 : nz, op->row_begin, op->nloc, plane};
+    op->geom = make_stencil_geom(dims, nx, ny, nz, op->row_begin, op->nloc);
     if (ctx.nranks > 1) {
         op->halo_lo.ensure(static_cast<size_t>(plane) * 8);
         op->halo_hi.ensure(static_cast<size_t>(plane) * 8);

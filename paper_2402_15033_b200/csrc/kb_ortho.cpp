@@ -59,7 +59,7 @@ void gram_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double
                 const double val = h[off + e];
                 if (j >= w) continue;
                 if (mrow < wslots) {
-                    if (mrow <= j) g(mrow, j) = val;
+                    if (gi == 0 && mrow <= j) g(mrow, j) = val;  // later groups skip VᵀV
                 } else {
                     const i64 l = mrow - wslots;
                     if (l < cp) r_col(start + l, j) = val;
@@ -85,13 +85,16 @@ void update_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const doub
     ctx.coef.ensure(total * 8);
     double* hc = ctx.h_coef.p;
     std::memset(hc, 0, total * 8);
+    // Column slot of j in a coefficient row: natural order, or for the
+    // two-threads-per-row kernel (wmax 64) even columns then odd columns.
+    auto slot = [wmax](i64 j) -> i64 { return wmax == 64 ? (j & 1) * 32 + (j >> 1) : j; };
     for (i64 l = 0; l < c0; ++l)
-        for (i64 j = 0; j < w; ++j) hc[l * wmax + j] = -r_col(l, j);
+        for (i64 j = 0; j < w; ++j) hc[l * wmax + slot(j)] = -r_col(l, j);
     double* nrjj = hc + c0 * wmax;
     double* inv = nrjj + static_cast<size_t>(wmax) * wmax;
     for (i64 j = 0; j < w; ++j) {
-        for (i64 l = 0; l < j; ++l) nrjj[l * wmax + j] = triangular ? -r_jj(l, j) : 0.0;
-        inv[j] = triangular ? 1.0 / r_jj(j, j) : 1.0;
+        for (i64 l = 0; l < j; ++l) nrjj[l * wmax + slot(j)] = triangular ? -r_jj(l, j) : 0.0;
+        inv[slot(j)] = triangular ? 1.0 / r_jj(j, j) : 1.0;
     }
     cudaEvent_t t0 = ctx.begin_phase();
     KB_CUDA(cudaMemcpyAsync(ctx.coef.p, hc, total * 8, cudaMemcpyHostToDevice, ctx.stream));

@@ -41,7 +41,7 @@ METRIC = "GMRES time-to-solution (s) & BlkOrtho HBM GB/s, 2D Laplace, 1/2/4/8 B2
 def parse():
     p = argparse.ArgumentParser()
     p.add_argument("--gpus", type=int, default=1)
-    p.add_argument("--steps", type=int, default=5)
+    p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--grid", type=int, default=4000, help="grid side per GPU (rows per GPU = grid²)")

@@ -84,16 +84,23 @@ def available() -> bool:
     return os.path.exists(REF_LIB)
 
 
+def _load(path):
+    L = C.CDLL(path)
+    for k, (r, a) in SIGS.items():
+        f = getattr(L, k)
+        f.restype, f.argtypes = r, a
+    return L
+
+
 def lib():
     global _lib
     if _lib is None:
+        if os.environ.get("KRY_REF_VARIANT") == "fma":  # rounding-envelope measurement only
+            _lib = _load(os.path.join(HERE, "_ref", "libkrylov_ref_fma.so"))
+            return _lib
         if not available():
             raise FileNotFoundError(f"{REF_LIB} not built (make -C oracle ref)")
-        L = C.CDLL(REF_LIB)
-        for k, (r, a) in SIGS.items():
-            f = getattr(L, k)
-            f.restype, f.argtypes = r, a
-        _lib = L
+        _lib = _load(REF_LIB)
     return _lib
 
 

@@ -431,6 +431,85 @@ __global__ void __launch_bounds__(256)
 }
 
 // ---------------------------------------------------------------------------
+// K5b: update as a tall-skinny DMMA GEMM,  out = [V | P] · M  with
+//   M = [[R_jj⁻¹]; [−R_col·R_jj⁻¹]]  (slots × wslots, R_jj⁻¹ upper triangular).
+// Used only when R_jj is well conditioned (κ_F ≤ 4w) — the second-stage
+// finalize and second passes, where the panel is already nearly orthonormal
+// and R_jj ≈ I — so the explicit inverse loses nothing against substitution
+// while the 1830-FMA/row substitution moves onto the DMMA pipe.  [V | P] is
+// staged through the same TMA ring as the Gram (rows ≡ 4 mod 16: the A
+// fragment loads X[r0 + lane/4][4kc + lane%4] are conflict-free); M lives in
+// shared memory in fragment order, mfrag[(kc·NBW + jb)·32 + lane] =
+// M[4kc + lane%4][8jb + lane/4].  Chunks are 8 rows (the MMA m dimension);
+// the last chunk of a tile overhangs it and its extra rows are discarded.
+// ---------------------------------------------------------------------------
+template <int NBW, int NB, int CW = 8>
+__global__ void __launch_bounds__((CW + 1) * 32, 1)
+    update_mma_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_p,
+                      const TsParams p, const double* __restrict__ mfrag, double* out, i64 ldo) {
+    constexpr int KC = 2 * NB;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    uint64_t *full, *empty;
+    double* ring = ring_setup(smem, p, full, empty);
+    const size_t stage_doubles = static_cast<size_t>(p.wslots + p.cpslots) * p.tr;
+    double* msm = reinterpret_cast<double*>(smem + stage_doubles * 8 * p.stages + 16 * p.stages + 1024);
+    msm = reinterpret_cast<double*>((reinterpret_cast<uintptr_t>(msm) + 127) & ~uintptr_t(127));
+    for (int i = threadIdx.x; i < KC * NBW * 32; i += blockDim.x) msm[i] = mfrag[i];
+    __syncthreads();
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    if (warp == CW) {
+        if (lane == 0) ring_produce(&map_v, &map_p, p, ring, full, empty);
+        return;
+    }
+    const int m = lane >> 2, kq = lane & 3;
+    const int nchunks = (p.tr + 7) / 8;
+    int s = 0, use = 0, rot = warp;
+    for (i64 tile = blockIdx.x; tile < p.ntiles; tile += gridDim.x) {
+        mbar_wait(&full[s], use & 1);
+        const double* st = ring + s * stage_doubles;
+        for (int c = rot; c < nchunks; c += CW) {
+            const int r = 8 * c + m;
+            double a[KC];
+#pragma unroll
+            for (int kc = 0; kc < KC; ++kc) a[kc] = st[static_cast<size_t>(4 * kc + kq) * p.tr + r];
+            const i64 row = tile * p.tr + r;
+            const bool ok = r < p.tr && row < p.n;
+#pragma unroll
+            for (int jb = 0; jb < NBW; ++jb) {
+                double d0 = 0.0, d1 = 0.0;
+#pragma unroll
+                for (int kc = 0; kc < KC; ++kc)
+                    if (kc < 2 * (jb + 1) || kc >= 2 * NBW) dmma(d0, d1, a[kc], msm[(kc * NBW + jb) * 32 + lane]);
+                const int col = 8 * jb + 2 * kq;
+                if (ok) {
+                    if (col < p.w) out[row + col * ldo] = d0;
+                    if (col + 1 < p.w) out[row + (col + 1) * ldo] = d1;
+                }
+            }
+        }
+        __syncwarp();
+        if (lane == 0) mbar_arrive(&empty[s]);
+        rot = (rot + 1) & (CW - 1);
+        if (++s == p.stages) {
+            s = 0;
+            ++use;
+        }
+    }
+}
+
+template <int NBW, int NB>
+const void* update_mma_fn(int nbw, int nb) {
+    if (nbw == NBW && nb == NB) return reinterpret_cast<const void*>(update_mma_kernel<NBW, NB>);
+    if constexpr (NB < 8) {
+        return update_mma_fn<NBW, NB + 1>(nbw, nb);
+    } else if constexpr (NBW < 8) {
+        return update_mma_fn<NBW + 1, NBW + 1>(nbw, nb);
+    } else {
+        return nullptr;
+    }
+}
+
+// ---------------------------------------------------------------------------
 // Host side: tensor maps, geometry, launches.
 // ---------------------------------------------------------------------------
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
@@ -568,6 +647,28 @@ void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 
     gram_reduce_kernel<<<ceil_div(per_cta * 32, 256), 256, 0, stream>>>(d_partials, grid, per_cta, d_packed);
     KB_LAUNCHED();
     launches += 2;
+}
+
+void launch_update_mma(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
+                       i64 w, const double* d_mfrag, double* out, i64 ldo, int64_t& launches) {
+    TsParams p = geometry(n, static_cast<int>(w), static_cast<int>(cp), true);
+    const int nbw = p.wslots / 8, nb = nbw + p.cpslots / 8;
+    if (nb > 8) fail(KRY_INTERNAL, "update_mma shape");
+    p.consumers = 8;
+    const size_t mbytes = static_cast<size_t>(2 * nb) * nbw * 32 * 8;
+    const size_t stage_bytes = static_cast<size_t>(p.wslots + p.cpslots) * p.tr * 8;
+    p.stages = std::max(2, std::min(p.stages, static_cast<int>((200 * 1024 - mbytes) / stage_bytes)));
+    const size_t smem = ring_bytes(p) + 1024 + 128 + mbytes + 256;
+    CUtensorMap mv = make_map(V, ldv, n, w, p.tr);
+    CUtensorMap mp = make_map(P, ldp, n, cp, p.tr);
+    const int grid = static_cast<int>(std::min<i64>(sm_count(), std::max<i64>(1, p.ntiles)));
+    const void* fn = update_mma_fn<1, 1>(nbw, nb);
+    if (!fn) fail(KRY_UNSUPPORTED, "update_mma shape");
+    set_smem(fn, smem);
+    void* args[] = {&mv, &mp, &p, &d_mfrag, &out, &ldo};
+    KB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(9 * 32), args, smem, stream));
+    KB_LAUNCHED();
+    launches += 1;
 }
 
 int update_wmax(i64 w) { return w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64; }

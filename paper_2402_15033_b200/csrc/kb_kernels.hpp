@@ -20,6 +20,10 @@ void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 
                       i64 ldv, i64 w, bool vv, double* d_partials, double* d_packed,
                       std::vector<int>& tile_ids, int64_t& launches);
 int update_wmax(i64 w);
+// out = [V | P]·M on DMMA; d_mfrag holds M in fragment order (k_tsqr.cu, K5b).
+// Requires round_up(w,8) + round_up(cp,8) ≤ 64.
+void launch_update_mma(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
+                       i64 w, const double* d_mfrag, double* out, i64 ldo, int64_t& launches);
 // out = (V − P·R_col)·R_jj⁻¹ (triangular) or V − P·R_col; out may alias V.
 void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
                    i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches);

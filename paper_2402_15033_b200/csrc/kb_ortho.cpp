@@ -1,6 +1,7 @@
 #include "kb_ortho.hpp"
 
 #include <algorithm>
+#include <cmath>
 #include <cstring>
 
 #include "kb_kernels.hpp"
@@ -79,6 +80,54 @@ void update_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const doub
             if (r_jj(j, j) == 0.0) fail(KRY_SINGULAR_FACTOR, "triangular factor has a zero diagonal entry");
     if (round_up(w, 8) > 64)
         fail(KRY_UNSUPPORTED, "block width above 64 columns is not supported on the device path");
+    if (triangular && w >= 17 && round_up(w, 8) + round_up(c0, 8) <= 64) {
+        // Wide, well-conditioned R_jj (finalize / second pass): substitution
+        // as a DMMA GEMM against the explicit inverse (k_tsqr.cu, K5b).
+        Upper rinv(w);
+        for (i64 j = 0; j < w; ++j) {
+            rinv.at(j, j) = 1.0 / r_jj(j, j);
+            for (i64 i = j - 1; i >= 0; --i) {
+                double s = 0.0;
+                for (i64 k = i; k < j; ++k) s += rinv(i, k) * r_jj(k, j);
+                rinv.at(i, j) = -s / r_jj(j, j);
+            }
+        }
+        double nr = 0.0, ni = 0.0;
+        for (i64 j = 0; j < w; ++j)
+            for (i64 i = 0; i <= j; ++i) {
+                nr += r_jj(i, j) * r_jj(i, j);
+                ni += rinv(i, j) * rinv(i, j);
+            }
+        if (std::sqrt(nr * ni) <= 4.0 * w) {
+            const i64 wslots = round_up(w, 8), nbw = wslots / 8, nb = nbw + round_up(c0, 8) / 8;
+            const size_t total = static_cast<size_t>(2 * nb) * nbw * 32;
+            ctx.h_coef.ensure(total * 8);
+            ctx.coef.ensure(total * 8);
+            double* hm = ctx.h_coef.p;
+            // M row k: V slot k < wslots → R⁻¹(k, :); P slot → −(R_col·R⁻¹)(k − wslots, :).
+            auto mval = [&](i64 k, i64 j) -> double {
+                if (j >= w) return 0.0;
+                if (k < wslots) return (k < w && k <= j) ? rinv(k, j) : 0.0;
+                const i64 l = k - wslots;
+                if (l >= c0) return 0.0;
+                double s = 0.0;
+                for (i64 t = 0; t <= j; ++t) s += r_col(l, t) * rinv(t, j);
+                return -s;
+            };
+            for (i64 kc = 0; kc < 2 * nb; ++kc)
+                for (i64 jb = 0; jb < nbw; ++jb)
+                    for (int lane = 0; lane < 32; ++lane)
+                        hm[(kc * nbw + jb) * 32 + lane] = mval(4 * kc + (lane & 3), 8 * jb + (lane >> 2));
+            cudaEvent_t t0 = ctx.begin_phase();
+            KB_CUDA(cudaMemcpyAsync(ctx.coef.p, hm, total * 8, cudaMemcpyHostToDevice, ctx.stream));
+            launch_update_mma(ctx.stream, n, c0 > 0 ? P : nullptr, ldp, c0, V, ldv, w, ctx.coef.p, out, ldo,
+                              ctx.launches);
+            ctx.end_phase(PH_UPDATE, t0);
+            ctx.update_bytes += 8.0 * n * (c0 + 2.0 * w);
+            ctx.update_launches += 1;
+            return;
+        }
+    }
     const int wmax = update_wmax(w);
     const size_t total = static_cast<size_t>(c0 + wmax + 1) * wmax;
     ctx.h_coef.ensure(total * 8);

@@ -164,6 +164,11 @@ int kry_operator_create_csr(kry_ctx* ctx, int64_t n_global, int64_t row_begin, i
  * whole grid lines (2D) / planes (3D) across the context's ranks. */
 int kry_operator_create_laplace2d(kry_ctx* ctx, int64_t nx, int64_t ny, kry_operator** out);
 int kry_operator_create_laplace3d(kry_ctx* ctx, int64_t nx, int64_t ny, int64_t nz, kry_operator** out);
+/* Host-only: the rows a rank owns under the matrix-free operators' partition
+ * (whole grid lines in 2D, whole planes in 3D; dims = 2 or 3, nz ignored for
+ * 2D) and the halo length it exchanges with each neighbour.  No device use. */
+int kry_laplace_partition(int dims, int64_t nx, int64_t ny, int64_t nz, int nranks, int rank, int64_t* row_begin,
+                          int64_t* n_local, int64_t* halo);
 int kry_operator_destroy(kry_operator* op);
 int kry_operator_rows(const kry_operator* op, int64_t* n_global, int64_t* row_begin, int64_t* n_local);
 int kry_operator_nnz(const kry_operator* op, int64_t* nnz_local);

@@ -84,6 +84,7 @@ SIGNATURES = {
     "kry_operator_create_csr": (C.c_int, [vp, i64, i64, i64, P_i64, P_i64, P_dbl, C.POINTER(vp)]),
     "kry_operator_create_laplace2d": (C.c_int, [vp, i64, i64, C.POINTER(vp)]),
     "kry_operator_create_laplace3d": (C.c_int, [vp, i64, i64, i64, C.POINTER(vp)]),
+    "kry_laplace_partition": (C.c_int, [C.c_int, i64, i64, i64, C.c_int, C.c_int, P_i64, P_i64, P_i64]),
     "kry_operator_destroy": (C.c_int, [vp]),
     "kry_operator_rows": (C.c_int, [vp, P_i64, P_i64, P_i64]),
     "kry_operator_nnz": (C.c_int, [vp, P_i64]),

@@ -311,6 +311,18 @@ int kry_operator_create_laplace3d(kry_ctx* ctx, int64_t nx, int64_t ny, int64_t 
     });
 }
 
+int kry_laplace_partition(int dims, int64_t nx, int64_t ny, int64_t nz, int nranks, int rank, int64_t* row_begin,
+                          int64_t* n_local, int64_t* halo) {
+    return guarded([&] {
+        if (dims != 2 && dims != 3) kb::fail(KRY_INVALID_ARGUMENT, "dims must be 2 or 3");
+        i64 rb = 0, nl = 0, h = 0;
+        kb::laplace_partition(dims, nx, ny, dims == 2 ? 1 : nz, nranks, rank, rb, nl, h);
+        *row_begin = rb;
+        *n_local = nl;
+        *halo = h;
+    });
+}
+
 int kry_operator_destroy(kry_operator* op) {
     return guarded([&] {
         if (!op) return;

@@ -13,6 +13,20 @@ namespace kb {
             ::kb::fail(KRY_NCCL_ERROR, std::string(#expr) + ": " + ncclGetErrorString(kb_r_)); \
     } while (0)
 
+void laplace_partition(int dims, i64 nx, i64 ny, i64 nz, int nranks, int rank, i64& row_begin, i64& nloc,
+                       i64& halo) {
+    // 1D block-row partition by whole grid lines / planes:
+    // rank r owns lines [r·L/P, (r+1)·L/P); the halo is one line / plane.
+    const i64 lines = dims == 2 ? ny : nz;
+    const i64 plane = dims == 2 ? nx : nx * ny;
+    if (nranks < 1 || rank < 0 || rank >= nranks) fail(KRY_INVALID_ARGUMENT, "bad rank layout");
+    if (lines < nranks) fail(KRY_INVALID_ARGUMENT, "fewer grid lines than ranks");
+    const i64 l0 = rank * lines / nranks, l1 = (rank + 1) * lines / nranks;
+    row_begin = l0 * plane;
+    nloc = (l1 - l0) * plane;
+    halo = nranks > 1 ? plane : 0;
+}
+
 Operator* make_laplace(Ctx& ctx, int dims, i64 nx, i64 ny, i64 nz) {
     if (dims == 2) {
         if (nx < 2 || ny < 2) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: gen_laplace2d needs dimensions >= 2");
@@ -23,21 +37,19 @@ Operator* make_laplace(Ctx& ctx, int dims, i64 nx, i64 ny, i64 nz) {
     auto* op = new Operator;
     op->ctx = &ctx;
     op->kind = dims == 2 ? Operator::LAPLACE2D : Operator::LAPLACE3D;
-    const i64 lines = dims == 2 ? ny : nz;
-    const i64 plane = dims == 2 ? nx : nx * ny;
-    if (lines < ctx.nranks) {
+    i64 halo = 0;
+    try {
+        laplace_partition(dims, nx, ny, nz, ctx.nranks, ctx.rank, op->row_begin, op->nloc, halo);
+    } catch (...) {
         delete op;
-        fail(KRY_INVALID_ARGUMENT, "fewer grid lines than ranks");
+        throw;
     }
-    const i64 l0 = ctx.rank * lines / ctx.nranks, l1 = (ctx.rank + 1) * lines / ctx.nranks;
-    op->n_global = plane * lines;
-    op->row_begin = l0 * plane;
-    op->nloc = (l1 - l0) * plane;
+    op->n_global = dims == 2 ? nx * ny : nx * ny * nz;
     op->nnz_local = 0;
     op->geom = make_stencil_geom(dims, nx, ny, nz, op->row_begin, op->nloc);
     if (ctx.nranks > 1) {
-        op->halo_lo.ensure(static_cast<size_t>(plane) * 8);
-        op->halo_hi.ensure(static_cast<size_t>(plane) * 8);
+        op->halo_lo.ensure(static_cast<size_t>(halo) * 8);
+        op->halo_hi.ensure(static_cast<size_t>(halo) * 8);
     }
     op->partials.ensure(static_cast<size_t>(stencil_partials(op->geom) + 64) * 8);
     return op;
@@ -70,7 +82,8 @@ Operator* make_csr(Ctx& ctx, i64 n_global, i64 row_begin, i64 nloc, const int64_
     if (ctx.nranks > 1) {
         DevBuf d;
         d.ensure(layout.size() * 8);
-        KB_CUDA(cudaMemcpyAsync(d.p, layout.data() + 2 * ctx.rank, 16, cudaMemcpyHostToDevice, ctx.stream));
+        KB_CUDA(cudaMemcpyAsync(d.as<int64_t>() + 2 * ctx.rank, layout.data() + 2 * ctx.rank, 16,
+                                cudaMemcpyHostToDevice, ctx.stream));
         KB_NCCL(ncclAllGather(d.as<int64_t>() + 2 * ctx.rank, d.as<int64_t>(), 2, ncclInt64, ctx.comm,
                               ctx.stream));
         KB_CUDA(cudaMemcpyAsync(layout.data(), d.p, layout.size() * 8, cudaMemcpyDeviceToHost, ctx.stream));

@@ -30,6 +30,8 @@ struct Operator {
     double bytes_per_apply() const;
 };
 
+void laplace_partition(int dims, i64 nx, i64 ny, i64 nz, int nranks, int rank, i64& row_begin, i64& nloc,
+                       i64& halo);
 Operator* make_laplace(Ctx& ctx, int dims, i64 nx, i64 ny, i64 nz);
 Operator* make_csr(Ctx& ctx, i64 n_global, i64 row_begin, i64 nloc, const int64_t* row_ptr,
                    const int64_t* col_idx, const double* vals);

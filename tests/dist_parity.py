@@ -1,0 +1,78 @@
+"""Multi-GPU parity driver (launched by tests/test_gpu_multi.py under torchrun).
+
+Each rank owns a contiguous block of grid lines (kry_laplace_partition); the
+solver exchanges halos with NCCL send/recv and allreduces one packed Gram per
+BCGS-PIP (+ one scalar per norm).  The run must reproduce the reference's
+golden SolveReport exactly in status / iterations / restarts / reduces /
+SyncCounter deltas and within the §8(c) tolerance per cycle, on every rank.
+Prints one JSON line per rank; exit code 0 iff all configs pass."""
+import json
+import os
+import sys
+
+import numpy as np
+import torch
+import torch.distributed as dist
+
+ROOT = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+sys.path.insert(0, ROOT)
+sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
+
+import paper_2402_15033_b200 as kb  # noqa: E402
+
+GOLDEN = json.load(open(os.path.join(ROOT, "tests", "golden", "solver_golden.json")))
+CONFIGS = ["two_2d100_s60", "two_2d100_s20", "pip2_2d64", "two_3d16_s60", "two_2d48_csr", "standard_2d32",
+           "two_2d128_s60"]
+
+
+def main():
+    rank, world = int(os.environ["RANK"]), int(os.environ["WORLD_SIZE"])
+    local = int(os.environ.get("LOCAL_RANK", rank))
+    torch.cuda.set_device(local)
+    dist.init_process_group("nccl", device_id=torch.device(f"cuda:{local}"))
+    idb = torch.zeros(kb.lib().kry_nccl_unique_id_size(), dtype=torch.uint8, device="cuda")
+    if rank == 0:
+        idb.copy_(torch.frombuffer(bytearray(kb.Context.nccl_unique_id()), dtype=torch.uint8))
+    dist.broadcast(idb, 0)
+    ctx = kb.Context(local, world, rank, bytes(idb.cpu().tolist()))
+    from test_gpu_solver import cycle_tolerance  # same tolerance as the 1-GPU tests
+    results, ok = {}, True
+    for key in CONFIGS:
+        g = GOLDEN[key]
+        grid = g["grid"]
+        if g["operator"] == "csr":
+            from oracle import ref
+            a = ref.laplace2d(grid, grid)
+            n = a.n
+            rb, re = rank * n // world, (rank + 1) * n // world
+            rp = a.row_ptr[rb:re + 1] - a.row_ptr[rb]
+            ci = a.col_idx[a.row_ptr[rb]:a.row_ptr[re]]
+            vv = a.vals[a.row_ptr[rb]:a.row_ptr[re]]
+            op = kb.CsrOperator(rp, ci, vv, n_global=n, row_begin=rb, ctx=ctx)
+        elif g["dims"] == 2:
+            op = kb.Laplace2D(grid, grid, ctx)
+        else:
+            op = kb.Laplace3D(grid, grid, grid, ctx)
+        b = op.spmv(np.ones(op.n))
+        cfg = kb.SolverConfig(scheme=kb.OrthoScheme(kb.OrthoKind(g["kind"]), g["shat"]), big_step=g["shat"],
+                              max_iters=g["max_iters"])
+        rep = kb.standard_gmres(op, b, None, cfg) if g["standard"] else kb.sstep_gmres(op, b, None, cfg)
+        got, want = np.array(rep.cycle_residuals), np.array(g["cycle_residuals"])
+        counts = (int(rep.status), rep.iterations, rep.restarts, rep.sync.reduces) == (
+            g["status"], g["iterations"], g["restarts"], g["reduces"])
+        deltas = rep.sync.per_block == g["per_block"] and rep.sync.per_big_panel == g["per_big_panel"]
+        cyc = got.shape == want.shape and bool(np.all(np.abs(got - want) <= cycle_tolerance(g)))
+        results[key] = {"counts": counts, "deltas": deltas, "cycles": cyc, "rows": [op.row_begin, op.n],
+                        "allreduces": rep.telemetry["allreduces"],
+                        "max_rel_cycle_diff": float(np.max(np.abs(got - want) / want)) if got.shape == want.shape
+                        else None}
+        ok = ok and counts and deltas and cyc
+        del op
+    print(json.dumps({"rank": rank, "world": world, "ok": ok, "results": results}), flush=True)
+    ctx.close()
+    dist.destroy_process_group()
+    return 0 if ok else 1
+
+
+if __name__ == "__main__":
+    sys.exit(main())

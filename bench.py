@@ -47,7 +47,8 @@ def parse():
     p.add_argument("--grid", type=int, default=4000, help="grid side per GPU (rows per GPU = grid²)")
     p.add_argument("--shat", type=int, default=60)
     p.add_argument("--scheme", choices=["two-stage", "bcgs-pip2"], default="two-stage")
-    p.add_argument("--tts", action="store_true", help="also measure a full time-to-solution solve (N=1)")
+    p.add_argument("--tts", action="store_true", help="also run a full solve at the bench grid (N=1)")
+    p.add_argument("--no-tts512", action="store_true", help="skip the 512² time-to-solution solves")
     p.add_argument("--no-cpu-baseline", action="store_true")
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample-blocks", type=int, default=3)
@@ -342,6 +343,32 @@ def run_ours(args):
                "sample": desc + f"; {secs:.1f} s of CPU BlkOrtho ({byts / 1e9:.1f} GB algorithmic); V blocks "
                                 "from the bit-identical GPU MPK"}
 
+    # Time to solution at BASELINE config 1 (2D Laplace 512², tol 1e-6): full
+    # solves from x0 = 0, one-stage BCGS-PIP2 (the CPU reference's config) and
+    # two-stage ŝ = 60; inputs resident in HBM, wall clock around the call.
+    tts512 = None
+    if world == 1 and not args.no_tts512:
+        op5 = kb.Laplace2D(512, 512, ctx)
+        one5 = torch.ones(op5.n, dtype=torch.float64, device="cuda")
+        b5 = torch.empty_like(one5)
+        x5 = torch.zeros_like(one5)
+        torch.cuda.synchronize()
+        kb.lib().kry_spmv_device(ctx.handle, op5.handle, one5.data_ptr(), b5.data_ptr())
+        tts512 = {"grid": [512, 512], "rel_tol": 1e-6,
+                  "cpu_reference_seconds_survey": {"bcgs_pip2_1thread": 329.5, "two_stage_8threads": 239.4,
+                                                   "source": "BASELINE.md §2 (survey container, 8-core Xeon)"}}
+        for label, knd, sh in [("bcgs_pip2", kb.OrthoKind.BCGS_PIP2, 0), ("two_stage_shat60", kb.OrthoKind.TWO_STAGE, 60)]:
+            cfgf = kb.SolverConfig(scheme=kb.OrthoScheme(knd, sh), big_step=sh)
+            kb.sstep_gmres_device(op5, b5.data_ptr(), None, cfgf, x5.data_ptr())  # warm (module load, workspace)
+            torch.cuda.synchronize()
+            t0 = time.perf_counter()
+            rep = kb.sstep_gmres_device(op5, b5.data_ptr(), None, cfgf, x5.data_ptr())
+            torch.cuda.synchronize()
+            tts512[label] = {"seconds": time.perf_counter() - t0, "status": rep.status.name.lower(),
+                             "iterations": rep.iterations, "restarts": rep.restarts, "reduces": rep.sync.reduces,
+                             "final_relative_residual": rep.final_relative_residual}
+        del op5
+
     tts = None
     if args.tts and world == 1:
         x.zero_()
@@ -378,6 +405,8 @@ def run_ours(args):
                           "mpk": b_mpk / max(t_mpk, 1e-12) / 1e9},
             "iterations_per_step": iters / steps, "reduces_per_step": reduces / steps,
         }
+        if tts512 is not None:
+            line["time_to_solution_512"] = tts512
         if tts is not None:
             line["time_to_solution"] = tts
         print(json.dumps(line), flush=True)

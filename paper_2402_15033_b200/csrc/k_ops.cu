@@ -140,6 +140,81 @@ __global__ void __launch_bounds__(kBlock) stencil_kernel(const StencilGeom g, co
     }
 }
 
+// 2-D 5-point stencil, two adjacent columns per thread (nx even): one 16-byte
+// load of the next line per step, the current/previous lines carried in
+// registers, the horizontal neighbours x[i-1], x[i+2] taken from the
+// neighbouring lanes by shuffle (only lanes 0/31 touch memory for them).
+// Same per-row summation order as stencil_kernel (bit-identical).
+template <bool RESID>
+__global__ void __launch_bounds__(kBlock) stencil2d_vec_kernel(const StencilGeom g, const double* __restrict__ x,
+                                                               const double* __restrict__ halo_lo,
+                                                               const double* __restrict__ halo_hi,
+                                                               const double* __restrict__ b,
+                                                               double* __restrict__ y,
+                                                               double* __restrict__ partials) {
+    const i64 ix = 2 * (blockIdx.x * static_cast<i64>(kBlock) + threadIdx.x);
+    const i64 nx = g.nx;
+    const bool active = ix < nx;
+    const int lane = threadIdx.x & 31;
+    double sq = 0.0;
+    for (i64 lc = static_cast<i64>(blockIdx.y) * kLinesPerThread; lc < g.lines;
+         lc += static_cast<i64>(gridDim.y) * kLinesPerThread) {
+        const i64 lend = min(lc + kLinesPerThread, g.lines);
+        i64 gl = g.line0 + lc;
+        double2 down = make_double2(0.0, 0.0), cur = make_double2(0.0, 0.0);
+        if (active) {
+            if (gl > 0)
+                down = lc > 0 ? *reinterpret_cast<const double2*>(x + (lc - 1) * nx + ix)
+                              : *reinterpret_cast<const double2*>(halo_lo + ix);
+            cur = *reinterpret_cast<const double2*>(x + lc * nx + ix);
+        }
+#pragma unroll
+        for (int k = 0; k < kLinesPerThread; ++k) {
+            const i64 l = lc + k;
+            if (l >= lend) break;  // uniform across the block
+            const i64 i = l * nx + ix;
+            const bool has_up = gl + 1 < g.ny;
+            double2 up = make_double2(0.0, 0.0);
+            if (active && has_up)
+                up = l + 1 < g.lines ? *reinterpret_cast<const double2*>(x + i + nx)
+                                     : *reinterpret_cast<const double2*>(halo_hi + ix);
+            double left = __shfl_up_sync(0xffffffffu, cur.y, 1);
+            double right = __shfl_down_sync(0xffffffffu, cur.x, 1);
+            if (active) {
+                if (lane == 0 && ix > 0) left = x[i - 1];
+                if (lane == 31 && ix + 2 < nx) right = x[i + 2];
+                double s0 = 0.0, s1 = 0.0;
+                if (gl > 0) s0 = acc_term(s0, -1.0, down.x);
+                if (ix > 0) s0 = acc_term(s0, -1.0, left);
+                s0 = acc_term(s0, 4.0, cur.x);
+                s0 = acc_term(s0, -1.0, cur.y);
+                if (has_up) s0 = acc_term(s0, -1.0, up.x);
+                if (gl > 0) s1 = acc_term(s1, -1.0, down.y);
+                s1 = acc_term(s1, -1.0, cur.x);
+                s1 = acc_term(s1, 4.0, cur.y);
+                if (ix + 2 < nx) s1 = acc_term(s1, -1.0, right);
+                if (has_up) s1 = acc_term(s1, -1.0, up.y);
+                if (RESID) {
+                    const double2 bb = *reinterpret_cast<const double2*>(b + i);
+                    const double r0 = __dsub_rn(bb.x, s0), r1 = __dsub_rn(bb.y, s1);
+                    *reinterpret_cast<double2*>(y + i) = make_double2(r0, r1);
+                    sq = fma(r0, r0, sq);
+                    sq = fma(r1, r1, sq);
+                } else {
+                    *reinterpret_cast<double2*>(y + i) = make_double2(s0, s1);
+                }
+            }
+            down = cur;
+            cur = up;
+            ++gl;
+        }
+    }
+    if (RESID) {
+        const double t = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
 template <bool RESID>
 __global__ void __launch_bounds__(kBlock) csr_kernel(i64 nloc, const int64_t* __restrict__ row_ptr,
                                                      const int32_t* __restrict__ col,
@@ -237,6 +312,18 @@ int stencil_partials(const StencilGeom& g) {
 
 int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const double* halo_lo,
                    const double* halo_hi, const double* b, double* y, double* partials, int64_t& launches) {
+    auto a16 = [](const void* p) { return p == nullptr || (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (g.dims == 2 && (g.nx & 1) == 0 && a16(x) && a16(y) && a16(b) && a16(halo_lo) && a16(halo_hi)) {
+        dim3 grid = stencil_grid(g);
+        grid.x = static_cast<unsigned>(ceil_div(g.nx / 2, kBlock));
+        if (b)
+            stencil2d_vec_kernel<true><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+        else
+            stencil2d_vec_kernel<false><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+        KB_LAUNCHED();
+        ++launches;
+        return b ? static_cast<int>(grid.x * grid.y) : 0;
+    }
     const dim3 grid = stencil_grid(g);
     if (g.dims == 2) {
         if (b)

@@ -312,10 +312,18 @@ __global__ void __launch_bounds__(256)
         for (int j = 0; j < WMAX; ++j) acc[j] = (j < w) ? V[row + j * ldv] : 0.0;
         const double* prow = P + row;
         int l = 0;
-        for (; l + 4 <= cp; l += 4) {
-            double pv[4];
+        // Register double buffering: the next 4 prefix values are in flight
+        // while the current 4 are consumed (≈ 2× the bytes in flight per warp).
+        double pv[4];
+        if (cp >= 4) {
 #pragma unroll
-            for (int u = 0; u < 4; ++u) pv[u] = __ldg(prow + (l + u) * ldp);
+            for (int u = 0; u < 4; ++u) pv[u] = __ldg(prow + u * ldp);
+        }
+        for (; l + 4 <= cp; l += 4) {
+            const bool more = l + 8 <= cp;
+            double pn[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pn[u] = more ? __ldg(prow + (l + 4 + u) * ldp) : 0.0;
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
                 const double2* cr = reinterpret_cast<const double2*>(nrc + (l + u) * WMAX);
@@ -326,6 +334,8 @@ __global__ void __launch_bounds__(256)
                     acc[j + 1] = fma(c.y, pv[u], acc[j + 1]);
                 }
             }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) pv[u] = pn[u];
         }
         for (; l < cp; ++l) {
             const double pv = __ldg(prow + l * ldp);
@@ -671,7 +681,7 @@ void launch_update_mma(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64
     launches += 1;
 }
 
-int update_wmax(i64 w) { return w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64; }
+int update_wmax(i64 w) { return w <= 6 ? 6 : w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64; }
 
 void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
                    i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches) {
@@ -688,6 +698,7 @@ void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp,
                                             triangular ? 1 : 0, out, ldo);
     };
     switch (wmax) {
+        case 6: go(update_kernel<6>); break;
         case 8: go(update_kernel<8>); break;
         case 16: go(update_kernel<16>); break;
         case 32: go(update_kernel<32>); break;

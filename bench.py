@@ -34,6 +34,8 @@ import time
 
 ROOT = os.path.dirname(os.path.abspath(__file__))
 sys.path.insert(0, ROOT)
+# Keep stdout to the one JSON line (NCCL prints its version banner otherwise).
+os.environ.setdefault("NCCL_DEBUG", "WARN")
 
 METRIC = "GMRES time-to-solution (s) & BlkOrtho HBM GB/s, 2D Laplace, 1/2/4/8 B200"
 
@@ -44,7 +46,10 @@ def parse():
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--grid", type=int, default=4000, help="grid side per GPU (rows per GPU = grid²)")
+    p.add_argument("--grid", type=int, default=4000, help="grid side per GPU (rows per GPU = grid² in 2D)")
+    p.add_argument("--dims", type=int, choices=[2, 3], default=2, help="2D 5-point or 3D 7-point Laplacian")
+    p.add_argument("--global-grid", type=int, default=0,
+                   help="strong scaling: fixed global grid side (e.g. 8000 = BASELINE configs[2]) split over the ranks")
     p.add_argument("--shat", type=int, default=60)
     p.add_argument("--scheme", choices=["two-stage", "bcgs-pip2"], default="two-stage")
     p.add_argument("--tts", action="store_true", help="also run a full solve at the bench grid (N=1)")
@@ -228,8 +233,15 @@ def run_ours(args):
     stream = torch.cuda.ExternalStream(ctx.stream_handle())
 
     g = args.grid
-    nx, ny = g, g * world
-    op = kb.Laplace2D(nx, ny, ctx)
+    strong = args.global_grid > 0
+    if args.dims == 2:
+        nx, ny, nz = (args.global_grid, args.global_grid, 1) if strong else (g, g * world, 1)
+        op = kb.Laplace2D(nx, ny, ctx)
+        shape = f"2D Laplace 5-pt {nx}x{ny}"
+    else:
+        nx, ny, nz = (args.global_grid,) * 3 if strong else (g, g, g * world)
+        op = kb.Laplace3D(nx, ny, nz, ctx)
+        shape = f"3D Laplace 7-pt {nx}x{ny}x{nz}"
     n = op.n
     kind = kb.OrthoKind.TWO_STAGE if args.scheme == "two-stage" else kb.OrthoKind.BCGS_PIP2
     cfg_cycle = kb.SolverConfig(scheme=kb.OrthoScheme(kind, args.shat), big_step=args.shat if kind == 3 else 0,
@@ -327,13 +339,13 @@ def run_ours(args):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            key = f"{dom}@{nx}x{g}"
+            key = f"{dom}@{nx}x{g}" if args.dims == 2 and not strong else f"{dom}@{shape}/{world}"
             traffic = tj.get(key)
         except Exception:
             traffic = None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.dims == 2 and not strong:
         def gpu_mpk(start):
             return op.mpk(start, 5)
         bh = b.cpu().numpy()
@@ -384,11 +396,13 @@ def run_ours(args):
         steps = args.steps
         line = {
             "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": world, "steps": steps,
-            "warmup": args.warmup, "ms_per_step": 1e3 * t_el / steps, "higher_is_better": True, "scaling": "weak",
+            "warmup": args.warmup, "ms_per_step": 1e3 * t_el / steps, "higher_is_better": True,
+            "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (b = A*1, x0 = 0, then warm restarts)",
-            "config": {"workload": f"2D Laplace 5-pt {nx}x{ny} ({g}x{g} rows per GPU), s-step GMRES(60) s=5, "
+            "config": {"workload": f"{shape} ({n} rows per GPU), s-step GMRES(60) s=5, "
                                    f"{args.scheme} BlkOrtho shat={args.shat}",
-                       "grid": [nx, ny], "rows_per_gpu": n, "m": 60, "s": 5, "shat": args.shat,
+                       "grid": [nx, ny] if args.dims == 2 else [nx, ny, nz], "rows_per_gpu": n, "m": 60, "s": 5,
+                       "shat": args.shat,
                        "step": "one full restart cycle (60 iterations) through kry_sstep_gmres_device",
                        "parallelism": f"row-partitioned dp{world}", "l2": "inputs larger than L2 (basis 8*61*n B)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",

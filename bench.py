@@ -48,6 +48,10 @@ def parse():
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
     p.add_argument("--grid", type=int, default=4000, help="grid side per GPU (rows per GPU = grid² in 2D)")
     p.add_argument("--dims", type=int, choices=[2, 3], default=2, help="2D 5-point or 3D 7-point Laplacian")
+    p.add_argument("--workload", choices=["laplace", "random"], default="laplace",
+                   help="random = BASELINE configs[4] (CSR, ~30 nnz/row, Jacobi-scaled)")
+    p.add_argument("--random-rows", type=int, default=20_000_000, help="rows per GPU of the random workload")
+    p.add_argument("--random-nnz", type=int, default=30)
     p.add_argument("--global-grid", type=int, default=0,
                    help="strong scaling: fixed global grid side (e.g. 8000 = BASELINE configs[2]) split over the ranks")
     p.add_argument("--shat", type=int, default=60)
@@ -58,6 +62,37 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample-blocks", type=int, default=3)
     return p.parse_args()
+
+
+def random_sparse_rows(n_global, row_begin, n_local, per_row, seed=1, chunk=1 << 20):
+    """BASELINE configs[4]: nonsymmetric random sparse rows with `per_row`
+    entries (diagonal + per_row-1 distinct random columns), values uniform in
+    [-1, 1], diagonal 1 + Σ|off-diagonal| (strictly diagonally dominant, so
+    GMRES converges), Jacobi-scaled (each row divided by its diagonal — the
+    reference has no preconditioner hook, so the scaled operator is the
+    problem both solvers see).  Columns strictly increasing per row (CSR
+    contract, csr_matrix.hpp:25-38).  Returns int64 row_ptr (from 0), int64
+    global columns, fp64 values for rows [row_begin, row_begin+n_local)."""
+    import numpy as np
+    k = per_row - 1
+    nnz = n_local * per_row
+    col = np.empty(nnz, dtype=np.int64)
+    val = np.empty(nnz, dtype=np.float64)
+    span = max(1, (n_global - 1) // (k + 1))
+    for c0 in range(0, n_local, chunk):
+        m = min(chunk, n_local - c0)
+        rng = np.random.default_rng([seed, row_begin + c0])
+        rows = np.arange(row_begin + c0, row_begin + c0 + m, dtype=np.int64)[:, None]
+        offs = np.cumsum(rng.integers(1, span + 1, size=(m, k), dtype=np.int64), axis=1)  # distinct, < n_global
+        cols = np.concatenate([(rows + offs) % n_global, rows], axis=1)
+        vals = rng.uniform(-1.0, 1.0, size=(m, k))
+        diag = 1.0 + np.abs(vals).sum(axis=1)
+        vals = np.concatenate([vals / diag[:, None], np.ones((m, 1))], axis=1)
+        order = np.argsort(cols, axis=1, kind="stable")
+        col[c0 * per_row:(c0 + m) * per_row] = np.take_along_axis(cols, order, axis=1).reshape(-1)
+        val[c0 * per_row:(c0 + m) * per_row] = np.take_along_axis(vals, order, axis=1).reshape(-1)
+    row_ptr = np.arange(n_local + 1, dtype=np.int64) * per_row
+    return row_ptr, col, val
 
 
 def peaks():
@@ -234,7 +269,15 @@ def run_ours(args):
 
     g = args.grid
     strong = args.global_grid > 0
-    if args.dims == 2:
+    if args.workload == "random":
+        nl = args.random_rows
+        n_glob = nl * world
+        rp, ci, vv = random_sparse_rows(n_glob, rank * nl, nl, args.random_nnz)
+        op = kb.CsrOperator(rp, ci, vv, n_global=n_glob, row_begin=rank * nl, ctx=ctx)
+        del rp, ci, vv
+        nx, ny, nz = n_glob, 1, 1
+        shape = f"random sparse n={n_glob} ({args.random_nnz} nnz/row, Jacobi-scaled)"
+    elif args.dims == 2:
         nx, ny, nz = (args.global_grid, args.global_grid, 1) if strong else (g, g * world, 1)
         op = kb.Laplace2D(nx, ny, ctx)
         shape = f"2D Laplace 5-pt {nx}x{ny}"
@@ -345,7 +388,8 @@ def run_ours(args):
             traffic = None
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.dims == 2 and not strong:
+    if (rank == 0 and world == 1 and not args.no_cpu_baseline and args.dims == 2 and not strong
+            and args.workload == "laplace"):
         def gpu_mpk(start):
             return op.mpk(start, 5)
         bh = b.cpu().numpy()

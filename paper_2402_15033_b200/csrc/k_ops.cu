@@ -215,6 +215,60 @@ __global__ void __launch_bounds__(kBlock) stencil2d_vec_kernel(const StencilGeom
     }
 }
 
+// CSR SpMV, one warp per 32 consecutive rows: the warp's contiguous nnz range
+// (values + int32 columns) is staged through shared memory with coalesced
+// loads in chunks of kCsrChunk entries, then each lane sums its own row
+// sequentially in stored order (bit-identical to spmv, csr_matrix.hpp:72-77)
+// — rows of ~30 entries no longer make every lane stride through memory.
+constexpr int kCsrChunk = 256;
+
+template <bool RESID>
+__global__ void __launch_bounds__(kBlock) csr_warp_kernel(i64 nloc, const int64_t* __restrict__ row_ptr,
+                                                          const int32_t* __restrict__ col,
+                                                          const double* __restrict__ vals,
+                                                          const double* __restrict__ x,
+                                                          const double* __restrict__ b, double* __restrict__ y,
+                                                          double* __restrict__ partials) {
+    __shared__ double s_val[kBlock / 32][kCsrChunk];
+    __shared__ int32_t s_col[kBlock / 32][kCsrChunk];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const i64 stride = static_cast<i64>(gridDim.x) * (kBlock / 32) * 32;
+    double sq = 0.0;
+    for (i64 r0 = (static_cast<i64>(blockIdx.x) * (kBlock / 32) + warp) * 32; r0 < nloc; r0 += stride) {
+        const i64 row = r0 + lane;
+        const bool live = row < nloc;
+        const i64 rs = live ? row_ptr[row] : 0, re = live ? row_ptr[row + 1] : 0;
+        const i64 last = (nloc - 1 - r0) < 31 ? (nloc - 1 - r0) : 31;
+        const i64 base = __shfl_sync(0xffffffffu, rs, 0);
+        const i64 end = __shfl_sync(0xffffffffu, re, static_cast<int>(last));
+        double s = 0.0;
+        for (i64 cs = base; cs < end; cs += kCsrChunk) {
+            const int cnt = static_cast<int>((end - cs) < kCsrChunk ? (end - cs) : kCsrChunk);
+            for (int k = lane; k < cnt; k += 32) {
+                s_val[warp][k] = vals[cs + k];
+                s_col[warp][k] = col[cs + k];
+            }
+            __syncwarp();
+            const i64 a0 = max(rs, cs), a1 = min(re, cs + cnt);
+            for (i64 k = a0; k < a1; ++k) s = acc_term(s, s_val[warp][k - cs], __ldg(x + s_col[warp][k - cs]));
+            __syncwarp();
+        }
+        if (live) {
+            if (RESID) {
+                const double r = __dsub_rn(b[row], s);
+                y[row] = r;
+                sq = fma(r, r, sq);
+            } else {
+                y[row] = s;
+            }
+        }
+    }
+    if (RESID) {
+        const double t = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.x] = t;
+    }
+}
+
 template <bool RESID>
 __global__ void __launch_bounds__(kBlock) csr_kernel(i64 nloc, const int64_t* __restrict__ row_ptr,
                                                      const int32_t* __restrict__ col,
@@ -343,11 +397,14 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
 
 int launch_csr(cudaStream_t s, i64 nloc, const int64_t* row_ptr, const int32_t* col, const double* vals,
                const double* x, const double* b, double* y, double* partials, int64_t& launches) {
-    const int grid = b ? reduce_grid() : grid_for(nloc);
+    // warp-staged kernel: 32 rows per warp, grid-stride (fixed grid in residual mode)
+    const i64 warps = ceil_div(nloc, 32);
+    const int grid = b ? reduce_grid()
+                       : static_cast<int>(std::max<i64>(1, std::min<i64>(ceil_div(warps, kBlock / 32), i64(1) << 30)));
     if (b)
-        csr_kernel<true><<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials);
+        csr_warp_kernel<true><<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials);
     else
-        csr_kernel<false><<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials);
+        csr_warp_kernel<false><<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials);
     KB_LAUNCHED();
     ++launches;
     return b ? grid : 0;

@@ -134,3 +134,23 @@ def test_zero_rhs_converges_immediately(kb, ctx):
     op = kb.Laplace2D(8, 8)
     rep = kb.sstep_gmres(op, np.zeros(64), None, kb.SolverConfig())
     assert rep.status == kb.SolveStatus.CONVERGED and rep.iterations == 0
+
+
+@pytest.mark.parametrize("kind,shat", [(3, 60), (2, 0)])
+def test_random_sparse_csr_parity(kb, ctx, ref, kind, shat):
+    """BASELINE configs[4] shape (~30 nnz/row, Jacobi-scaled) through the CSR
+    kernel: same counts as the live reference, cycle 1 within 1e-10."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import random_sparse_rows
+    n = 20000
+    rp, ci, vv = random_sparse_rows(n, 0, n, 30)
+    a = ref.Csr(n, rp, ci, vv)
+    b = ref.spmv(a, np.ones(n))
+    op = kb.CsrOperator(rp, ci, vv)
+    np.testing.assert_array_equal(op.spmv(np.ones(n)), b)  # bit-exact SpMV on ~30 nnz/row
+    want = ref.solve(a, b, None, ref.make_config(kind=kind, big_step=shat, shat=shat))
+    got = kb.sstep_gmres(op, b, None, kb.SolverConfig(scheme=kb.OrthoScheme(kb.OrthoKind(kind), shat), big_step=shat))
+    assert (int(got.status), got.iterations, got.restarts, got.sync.reduces) == (
+        want.status, want.iterations, want.restarts, want.reduces)
+    assert abs(got.cycle_residuals[0] - want.cycle_residuals[0]) <= 1e-10 * want.cycle_residuals[0] + ABS_FLOOR

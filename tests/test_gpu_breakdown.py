@@ -1,0 +1,68 @@
+"""Breakdown and stagnation paths of the restart loop against the live
+reference (gmres.hpp:315-343, 371-380; basis_store.hpp:178-208, 374-381)."""
+import numpy as np
+import pytest
+
+pytestmark = pytest.mark.gpu
+
+
+def csr_from_dense_pattern(n, entries):
+    rows = [[] for _ in range(n)]
+    for i, j, v in entries:
+        rows[i].append((j, v))
+    rp = np.zeros(n + 1, np.int64)
+    ci, vv = [], []
+    for i in range(n):
+        for j, v in sorted(rows[i]):
+            ci.append(j)
+            vv.append(v)
+        rp[i + 1] = len(ci)
+    return rp, np.array(ci, np.int64), np.array(vv)
+
+
+def run_both(kb, ref, rp, ci, vv, b, kind, shat=0, standard=False):
+    n = len(rp) - 1
+    a = ref.Csr(n, rp, ci, vv)
+    want = ref.solve(a, b, None, ref.make_config(kind=kind, big_step=shat, shat=shat), standard=standard)
+    op = kb.CsrOperator(rp, ci, vv)
+    cfg = kb.SolverConfig(scheme=kb.OrthoScheme(kb.OrthoKind(kind), shat), big_step=shat)
+    got = kb.standard_gmres(op, b, None, cfg) if standard else kb.sstep_gmres(op, b, None, cfg)
+    return got, want
+
+
+@pytest.mark.parametrize("kind,shat", [(2, 0), (3, 60), (3, 20), (1, 0)])
+def test_identity_operator_lucky_breakdown(kb, ctx, ref, kind, shat):
+    n = 300
+    rp, ci, vv = csr_from_dense_pattern(n, [(i, i, 1.0) for i in range(n)])
+    b = np.zeros(n)
+    b[7] = 1.0  # exact data: every Gram entry is exactly 1, so pivot 2 fails identically everywhere
+    got, want = run_both(kb, ref, rp, ci, vv, b, kind, shat)
+    assert (int(got.status), got.iterations, got.restarts, got.sync.reduces, got.breakdown) == (
+        want.status, want.iterations, want.restarts, want.reduces, want.breakdown)
+    assert got.breakdown and int(got.status) == 0  # converged by lucky breakdown
+    assert got.sync.per_block == [int(v) for v in want.per_block]
+    assert abs(got.breakdown_kappa - want.breakdown_kappa) <= 1e-6 * max(1.0, abs(want.breakdown_kappa))
+    np.testing.assert_allclose(got.solution, b, rtol=0, atol=1e-12)
+
+
+@pytest.mark.parametrize("kind,shat", [(2, 0), (3, 60)])
+def test_cyclic_shift_stagnates(kb, ctx, ref, kind, shat):
+    # GMRES(60) makes no progress on a 200-cycle until m ≥ n: two ≤1 % cycles → Stagnation
+    n = 200
+    rp, ci, vv = csr_from_dense_pattern(n, [(i, (i + 1) % n, 1.0) for i in range(n)])
+    b = np.zeros(n)
+    b[0] = 1.0
+    got, want = run_both(kb, ref, rp, ci, vv, b, kind, shat)
+    assert int(got.status) == want.status == 3  # SolveStatus::Stagnation
+    assert (got.iterations, got.restarts, got.sync.reduces) == (want.iterations, want.restarts, want.reduces)
+    np.testing.assert_allclose(got.cycle_residuals, want.cycle_residuals, rtol=1e-12)
+
+
+def test_standard_gmres_identity(kb, ctx, ref):
+    n = 100
+    rp, ci, vv = csr_from_dense_pattern(n, [(i, i, 2.0) for i in range(n)])
+    b = np.zeros(n)
+    b[3] = 2.0
+    got, want = run_both(kb, ref, rp, ci, vv, b, 1, standard=True)
+    assert (int(got.status), got.iterations, got.restarts, got.sync.reduces, got.breakdown) == (
+        want.status, want.iterations, want.restarts, want.reduces, want.breakdown)

@@ -299,53 +299,59 @@ __global__ void __launch_bounds__(256)
     // Columns w ≤ j < WMAX are identity padding (zero coefficients, inv = 1):
     // the arithmetic below is branch-free and leaves them at zero.
     extern __shared__ __align__(16) double c_sm[];
-    const int ncoef = (cp + WMAX + 1) * WMAX;
-    for (int i = threadIdx.x; i < ncoef; i += blockDim.x) c_sm[i] = coef[i];
+    // nrc rows zero-padded from cp to cpp = round_up(cp, 12) (the prefix loop
+    // runs in whole 12-column groups); then nrjj and inv.
+    const int cpp = (cp + 11) / 12 * 12;
+    for (int i = threadIdx.x; i < cpp * WMAX; i += blockDim.x) c_sm[i] = i < cp * WMAX ? coef[i] : 0.0;
+    for (int i = threadIdx.x; i < (WMAX + 1) * WMAX; i += blockDim.x)
+        c_sm[cpp * WMAX + i] = coef[cp * WMAX + i];
     __syncthreads();
     const double* nrc = c_sm;
-    const double* nrjj = c_sm + static_cast<size_t>(cp) * WMAX;
+    const double* nrjj = c_sm + static_cast<size_t>(cpp) * WMAX;
     const double* inv = nrjj + WMAX * WMAX;
     for (i64 row = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; row < n;
          row += static_cast<i64>(gridDim.x) * blockDim.x) {
         double acc[WMAX];
 #pragma unroll
         for (int j = 0; j < WMAX; ++j) acc[j] = (j < w) ? V[row + j * ldv] : 0.0;
+        // Prefix columns in batches of 4 through a 3-deep register ring: two
+        // batches (8 loads) are in flight while one is consumed.  The
+        // coefficient rows are zero-padded to a multiple of 12 (see the
+        // shared-memory fill), so there is no tail loop; loads past cp are
+        // predicated off.
         const double* prow = P + row;
-        int l = 0;
-        // Register double buffering: the next 4 prefix values are in flight
-        // while the current 4 are consumed (≈ 2× the bytes in flight per warp).
-        double pv[4];
-        if (cp >= 4) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) pv[u] = __ldg(prow + u * ldp);
-        }
-        for (; l + 4 <= cp; l += 4) {
-            const bool more = l + 8 <= cp;
-            double pn[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) pn[u] = more ? __ldg(prow + (l + 4 + u) * ldp) : 0.0;
+        const int nb = cpp / 4;
+        double b0[4], b1[4], b2[4];
+        auto ld = [&](double (&dst)[4], int bt) {
 #pragma unroll
             for (int u = 0; u < 4; ++u) {
-                const double2* cr = reinterpret_cast<const double2*>(nrc + (l + u) * WMAX);
+                const int l = 4 * bt + u;
+                dst[u] = l < cp ? __ldg(prow + static_cast<i64>(l) * ldp) : 0.0;
+            }
+        };
+        auto fm = [&](const double (&src)[4], int bt) {
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const double2* cr = reinterpret_cast<const double2*>(nrc + (4 * bt + u) * WMAX);
 #pragma unroll
                 for (int j = 0; j < WMAX; j += 2) {
                     const double2 c = cr[j / 2];
-                    acc[j] = fma(c.x, pv[u], acc[j]);
-                    acc[j + 1] = fma(c.y, pv[u], acc[j + 1]);
+                    acc[j] = fma(c.x, src[u], acc[j]);
+                    acc[j + 1] = fma(c.y, src[u], acc[j + 1]);
                 }
             }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) pv[u] = pn[u];
+        };
+        if (nb > 0) {
+            ld(b0, 0);
+            ld(b1, 1);
         }
-        for (; l < cp; ++l) {
-            const double pv = __ldg(prow + l * ldp);
-            const double2* cr = reinterpret_cast<const double2*>(nrc + l * WMAX);
-#pragma unroll
-            for (int j = 0; j < WMAX; j += 2) {
-                const double2 c = cr[j / 2];
-                acc[j] = fma(c.x, pv, acc[j]);
-                acc[j + 1] = fma(c.y, pv, acc[j + 1]);
-            }
+        for (int bt = 0; bt < nb; bt += 3) {  // nb is a multiple of 3
+            ld(b2, bt + 2);
+            fm(b0, bt);
+            ld(b0, bt + 3);
+            fm(b1, bt + 1);
+            ld(b1, bt + 4);
+            fm(b2, bt + 2);
         }
         if (triangular) {
             // Right-looking substitution: acc_j receives −R(k,j)·x_k for
@@ -686,7 +692,7 @@ int update_wmax(i64 w) { return w <= 6 ? 6 : w <= 8 ? 8 : w <= 16 ? 16 : w <= 32
 void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
                    i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches) {
     const int wmax = update_wmax(w);
-    const size_t smem = static_cast<size_t>(cp + wmax + 1) * wmax * 8;
+    const size_t smem = static_cast<size_t>(round_up(cp, 12) + wmax + 1) * wmax * 8;
     if (smem > 200 * 1024) fail(KRY_UNSUPPORTED, "update coefficients exceed shared memory");
     auto go = [&](auto kernel) {
         set_smem(reinterpret_cast<const void*>(kernel), smem);

@@ -3,6 +3,8 @@
 #include <chrono>
 #include <cmath>
 #include <limits>
+#include <cstdlib>
+#include <string>
 #include <utility>
 
 namespace kb {
@@ -117,6 +119,10 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         if (k == 0) return res;
         Mat h = assemble_hessenberg(store.coefficients(), k, store.block_records());
         Lsq lsq = solve_hessenberg_lsq(h, gamma);
+        // A deferred last-panel finalize: the same x update over the stored
+        // (preprocessed) columns with transformed coefficients.
+        std::vector<double> ycoef;
+        if (!store.deferred_coefficients(lsq.y, ycoef)) ycoef = lsq.y;
         res.implicit_crossed = lsq.implicit_residual <= cfg.rel_tol * r0;
         if (!res.implicit_crossed && !force) return res;
 
@@ -127,7 +133,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         for (i64 l0 = 0; l0 < lsq.valid_cols; l0 += 64) {
             Coef64 y{};
             const int cnt = static_cast<int>(std::min<i64>(64, lsq.valid_cols - l0));
-            for (int i = 0; i < cnt; ++i) y.v[i] = lsq.y[l0 + i];
+            for (int i = 0; i < cnt; ++i) y.v[i] = ycoef[l0 + i];
             launch_xupdate(ctx.stream, n, src, store.col(l0), store.ld(), cnt, y, xn.p, ctx.launches);
             src = xn.p;
         }
@@ -144,6 +150,10 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         return res;
     };
 
+    static const bool defer_last = [] {
+        const char* e = std::getenv("KRY_DEFER_FINALIZE");
+        return !(e && std::string(e) == "0");
+    }();
     bool done = false;
     int stagnation_strikes = 0;
     const i64 blocks = m / s;
@@ -199,7 +209,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
                 rep.breakdown_kappa = oc.kappa_estimate;
                 if (two_stage && store.big_panel_open()) {
                     cudaEvent_t t1 = ctx.begin_phase();
-                    store.finalize_big_panel(rep.sync);
+                    store.finalize_big_panel(rep.sync, defer_last);
                     ctx.end_phase(PH_ORTHO, t1);
                 }
                 Check res = check_and_update(gamma, true);
@@ -213,7 +223,9 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
                 const bool last_block = (j + 1 == blocks);
                 if (store.big_panel_full() || last_block) {
                     cudaEvent_t t1 = ctx.begin_phase();
-                    Outcome fin = store.finalize_big_panel(rep.sync);
+                    // The cycle's last panel is only read by the solution update:
+                    // defer its (15.6 GB at 4000²) rewrite into the y coefficients.
+                    Outcome fin = store.finalize_big_panel(rep.sync, defer_last && last_block);
                     ctx.end_phase(PH_ORTHO, t1);
                     if (fin.breakdown) {
                         rep.breakdown = true;

@@ -155,7 +155,7 @@ void update_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const doub
 }
 
 PipOut bcgs_pip_partial_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V,
-                               i64 ldv, i64 w, double* out, i64 ldo, i64& reduces) {
+                               i64 ldv, i64 w, double* out, i64 ldo, i64& reduces, bool do_update) {
     PipOut o;
     reduces += 1;  // fused [Q_prev, V]ᵀV (block_ortho.hpp:155)
     Mat s;
@@ -171,7 +171,12 @@ PipOut bcgs_pip_partial_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0
     }
     o.bad_pivot = try_cholesky(s, o.r_jj);
     if (o.bad_pivot != 0) return o;
-    update_device(ctx, n, P, ldp, c0, V, ldv, w, o.r_col, o.r_jj, out, ldo);
+    if (do_update) {
+        update_device(ctx, n, P, ldp, c0, V, ldv, w, o.r_col, o.r_jj, out, ldo);
+    } else {
+        for (i64 j = 0; j < w; ++j)  // tri_solve_right's check still applies to a deferred update
+            if (o.r_jj(j, j) == 0.0) fail(KRY_SINGULAR_FACTOR, "triangular factor has a zero diagonal entry");
+    }
     return o;
 }
 

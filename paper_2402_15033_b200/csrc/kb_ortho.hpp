@@ -26,6 +26,6 @@ void update_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const doub
 // bcgs_pip_partial: adds 1 to `reduces`; writes the block to `out` only when
 // the Pythagorean Cholesky succeeds (bad_pivot == 0).
 PipOut bcgs_pip_partial_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V,
-                               i64 ldv, i64 w, double* out, i64 ldo, i64& reduces);
+                               i64 ldv, i64 w, double* out, i64 ldo, i64& reduces, bool do_update = true);
 
 }  // namespace kb

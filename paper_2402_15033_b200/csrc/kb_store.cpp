@@ -25,7 +25,31 @@ Store::Store(Ctx& ctx, i64 n, i64 m, i64 panel_size, i64 big_panel_size)
     KB_CUDA(cudaMemsetAsync(q_.p, 0, static_cast<size_t>(ld_) * max_cols_ * 8, ctx_.stream));
 }
 
+bool Store::deferred_coefficients(const std::vector<double>& y, std::vector<double>& y_out) const {
+    if (!pending_) return false;
+    // Q_fin[:, c0+i] = (Q[:, c0:c0+w) − Q[:, 0:c0]·R_col)·R_jj⁻¹ column i; R_jj⁻¹ is
+    // upper triangular, so the first p panel columns only involve the first p.
+    const i64 k = static_cast<i64>(y.size());
+    y_out = y;
+    if (k <= pend_c0_) return true;
+    const i64 p = std::min(k - pend_c0_, pend_w_);
+    std::vector<double> z(static_cast<size_t>(p));
+    for (i64 i = p; i-- > 0;) {  // z = R_jj[:p,:p]⁻¹ · y_panel (back substitution)
+        double s = y[pend_c0_ + i];
+        for (i64 l = i + 1; l < p; ++l) s -= pend_rjj_(i, l) * z[l];
+        z[i] = s / pend_rjj_(i, i);
+    }
+    for (i64 l = 0; l < pend_c0_; ++l) {  // y_pre −= R_col[:, :p]·z
+        double s = 0.0;
+        for (i64 i = 0; i < p; ++i) s += pend_rcol_(l, i) * z[i];
+        y_out[l] = y[l] - s;
+    }
+    for (i64 i = 0; i < p; ++i) y_out[pend_c0_ + i] = z[i];
+    return true;
+}
+
 void Store::reset() {
+    pending_ = false;
     filled_ = 0;
     finalized_ = 0;
     big_panel_start_ = 0;
@@ -106,11 +130,12 @@ Outcome Store::append_impl(const double* V, i64 ldv, i64 w, bool overlap, int ki
 }
 
 Store::OrthoRes Store::pip(i64 c0, const double* V, i64 ldv, i64 w, double* out, i64 ldo, Sync& sync,
-                           bool first_pass) {
+                           bool first_pass, bool do_update) {
     i64 red = 0;
-    PipOut o = bcgs_pip_partial_device(ctx_, n_, col(0), ld_, c0, V, ldv, w, out, ldo, red);
+    PipOut o = bcgs_pip_partial_device(ctx_, n_, col(0), ld_, c0, V, ldv, w, out, ldo, red, do_update);
     sync.add(red);
-    ortho_bytes += 8.0 * n_ * (2.0 * c0 + 3.0 * w);
+    // algorithmic bytes actually moved: Gram reads c0+w; the update reads c0+w and writes w
+    ortho_bytes += do_update ? 8.0 * n_ * (2.0 * c0 + 3.0 * w) : 8.0 * n_ * (c0 + w);
     if (o.bad_pivot != 0) {
         if (first_pass) throw FirstPassFailure{o.bad_pivot};
         throw SecondPassBreakdown{o.bad_pivot};
@@ -271,15 +296,23 @@ void Store::commit(i64 c0, bool overlap, const OrthoRes& res, i64 w, int state) 
     records_.push_back(std::move(rec));
 }
 
-Outcome Store::finalize_big_panel(Sync& sync) {
+Outcome Store::finalize_big_panel(Sync& sync, bool deferred) {
     const i64 before = sync.reduces;
     Outcome out;
     if (!big_panel_open()) return out;
+    if (pending_) fail(KRY_INTERNAL, "a deferred finalize is still pending");
     const i64 c0 = big_panel_start_;
     const i64 w = filled_ - c0;
     OrthoRes res;
     try {
-        res = pip(c0, col(c0), ld_, w, col(c0), ld_, sync, true);
+        res = pip(c0, col(c0), ld_, w, col(c0), ld_, sync, true, /*do_update=*/!deferred);
+        if (deferred) {
+            pending_ = true;
+            pend_c0_ = c0;
+            pend_w_ = w;
+            pend_rcol_ = res.r_col;
+            pend_rjj_ = res.r_jj;
+        }
     } catch (const FirstPassFailure& e) {
         out.breakdown = true;
         out.pivot = e.pivot;

@@ -60,7 +60,14 @@ public:
     Outcome append_block(const double* V, i64 ldv, i64 w, bool overlap, int kind, i64 big_panel,
                          Sync& sync);
     Outcome preprocess_block(const double* V, i64 ldv, i64 w, bool overlap, Sync& sync);
-    Outcome finalize_big_panel(Sync& sync);
+    // `deferred`: leave Q[:, c0:filled) as the preprocessed panel and keep the
+    // finalize transform (R_col, R_jj) pending — valid only when nothing but
+    // the solution update reads the panel afterwards (the cycle's last panel).
+    Outcome finalize_big_panel(Sync& sync, bool deferred = false);
+    // Pending deferred finalize: x += Q_fin[:, 0:k]·y becomes the same
+    // update over the stored columns with y' = (y_pre − R_col·z, z),
+    // z = R_jj⁻¹·y_panel.  Returns false when nothing is pending.
+    bool deferred_coefficients(const std::vector<double>& y, std::vector<double>& y_out) const;
     // MPK into the store: column c0 holds the start; columns c0+1..c0+s.
     void mpk(Operator& op, i64 c0, i64 s);
 
@@ -82,7 +89,12 @@ private:
     Outcome append_impl(const double* V, i64 ldv, i64 w, bool overlap, int kind, Sync& sync);
     // Writes the orthonormal block into store columns [c0, c0+w).
     OrthoRes run_scheme(i64 c0, const double* V, i64 ldv, i64 w, int kind, Sync& sync);
-    OrthoRes pip(i64 c0, const double* V, i64 ldv, i64 w, double* out, i64 ldo, Sync& sync, bool first_pass);
+    OrthoRes pip(i64 c0, const double* V, i64 ldv, i64 w, double* out, i64 ldo, Sync& sync, bool first_pass,
+                 bool do_update = true);
+    bool pending_ = false;  // deferred finalize transform below applies to Q[:, pend_c0_:pend_c0_+pend_w_)
+    i64 pend_c0_ = 0, pend_w_ = 0;
+    Mat pend_rcol_;
+    Upper pend_rjj_;
     void commit(i64 c0, bool overlap, const OrthoRes& res, i64 w, int state);
     void combine_column(i64 col, i64 c0, i64 w, const OrthoRes& res);
     void combine_record(BlockRecord& rec, i64 c0, i64 w, const OrthoRes& res);

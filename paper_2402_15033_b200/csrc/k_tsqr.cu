@@ -93,6 +93,7 @@ struct TsParams {
     int stages;
     int vv;         // gram: compute the VᵀV tiles in this pass
     int consumers;  // consumer warps (empty-barrier arrival count)
+    int xb0;        // gram: first extra P slot block (NX > 0)
     int first;      // update: V holds the raw block (else the running partial)
     int last;       // update: apply the triangular solve and the scaling
     unsigned tx_bytes;
@@ -180,11 +181,15 @@ __host__ __device__ constexpr int tile_count(int nbw, int nb) {
 //   for both operands, so one LDS per block feeds every tile of the block.
 //   The smem column stride tr ≡ 4 (mod 16) makes those loads conflict-free.
 // ---------------------------------------------------------------------------
-template <int NBW, int NB, int CW = consumer_warps(NBW)>
+// NX > 0 (first-stage shapes only): additionally accumulate P_blocksᵀ·X for
+// the NX 8-column P blocks starting at block p.xb0 — the just-preprocessed
+// columns of the previous block, which the two-stage finalize needs
+// (Store::pgram_).  They ride on data this launch streams anyway.
+template <int NBW, int NB, int NX = 0, int CW = consumer_warps(NBW)>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
     gram_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_p,
                 const TsParams p, double* __restrict__ partials) {
-    constexpr int T = tile_count(NBW, NB);
+    constexpr int T = tile_count(NBW, NB) + NX * (NB - NBW);
     extern __shared__ __align__(1024) unsigned char smem[];
     uint64_t *full, *empty;
     double* ring = ring_setup(smem, p, full, empty);
@@ -201,6 +206,12 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     for (int jb = 0; jb < NBW; ++jb)
 #pragma unroll
         for (int ib = 0; ib < NB; ++ib) acc[jb][ib][0] = acc[jb][ib][1] = 0.0;
+    double accx[NX > 0 ? NX : 1][NB][2];
+#pragma unroll
+    for (int k = 0; k < (NX > 0 ? NX : 1); ++k)
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib) accx[k][ib][0] = accx[k][ib][1] = 0.0;
+    const int xb0 = p.xb0;
 
     const int frag_off = (lane >> 2) * p.tr + (lane & 3);
     const int nchunks = p.tr / 4;
@@ -222,6 +233,15 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
                     if (!tile_valid(NBW, jb, ib)) continue;
                     if (ib >= NBW || vv) dmma(acc[jb][ib][0], acc[jb][ib][1], f[ib], f[jb]);
                 }
+            if constexpr (NX > 0) {
+#pragma unroll
+                for (int k = 0; k < NX; ++k) {
+                    const double fx = base[static_cast<size_t>(8 * (xb0 + k)) * p.tr];
+#pragma unroll
+                    for (int ib = NBW; ib < NB; ++ib)
+                        if (ib <= xb0 + k) dmma(accx[k][ib][0], accx[k][ib][1], f[ib], fx);
+                }
+            }
         }
         __syncwarp();
         if (lane == 0) mbar_arrive(&empty[s]);
@@ -245,6 +265,17 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
             t[e0] = acc[jb][ib][0];
             t[e0 + 8] = acc[jb][ib][1];
         }
+    if constexpr (NX > 0) {  // extra tiles after the regular ones, (k, ib) order
+#pragma unroll
+        for (int k = 0; k < NX; ++k)
+#pragma unroll
+            for (int ib = NBW; ib < NB; ++ib) {
+                double* t = scratch +
+                            (static_cast<size_t>(warp) * T + tile_count(NBW, NB) + k * (NB - NBW) + (ib - NBW)) * 64;
+                t[e0] = accx[k][ib][0];
+                t[e0 + 8] = accx[k][ib][1];
+            }
+    }
     asm volatile("bar.sync 1, %0;" ::"n"(CW * 32));
     constexpr int per_cta = T * 64;
     double* out = partials + static_cast<size_t>(blockIdx.x) * per_cta;
@@ -280,6 +311,18 @@ const void* gram_fn(int nbw, int nb) {
     } else {
         return nullptr;
     }
+}
+
+// First-stage Gram (NBW = 1) with NX ∈ {1, 2} extra P-column blocks.
+template <int NB>
+const void* gram_x_fn(int nb, int nx) {
+    if (nb == NB) {
+        if (nx == 1) return reinterpret_cast<const void*>(gram_kernel<1, NB, 1>);
+        if (nx == 2) return reinterpret_cast<const void*>(gram_kernel<1, NB, 2>);
+        return nullptr;
+    }
+    if constexpr (NB < 8) return gram_x_fn<NB + 1>(nb, nx);
+    return nullptr;
 }
 
 // ---------------------------------------------------------------------------
@@ -637,7 +680,7 @@ i64 gram_scratch_doubles(i64 w) {
 
 void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V,
                       i64 ldv, i64 w, bool vv, double* d_partials, double* d_packed,
-                      std::vector<int>& tile_ids, int64_t& launches) {
+                      std::vector<int>& tile_ids, int64_t& launches, i64 x_first, i64 x_count) {
     TsParams p = geometry(n, static_cast<int>(w), static_cast<int>(cp), true);
     p.vv = vv ? 1 : 0;
     const int nbw = p.wslots / 8, nb = nbw + p.cpslots / 8;
@@ -645,6 +688,18 @@ void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 
     for (int jb = 0; jb < nbw; ++jb)
         for (int ib = 0; ib < nb; ++ib)
             if (tile_valid(nbw, jb, ib)) tile_ids.push_back(jb * 8 + ib);
+    // Extra P-column blocks (prefix columns [x_first, x_first + x_count)):
+    // tile id 64 + xb*8 + ib ↦ rows = slot block ib, cols = slot block xb.
+    int nx = 0;
+    p.xb0 = 0;
+    if (x_count > 0) {
+        const int s0 = p.wslots + static_cast<int>(x_first), s1 = s0 + static_cast<int>(x_count) - 1;
+        p.xb0 = s0 / 8;
+        nx = s1 / 8 - p.xb0 + 1;
+        if (nbw != 1 || nx > 2 || s1 / 8 >= nb) fail(KRY_INTERNAL, "gram extra-column shape");
+        for (int k = 0; k < nx; ++k)
+            for (int ib = nbw; ib < nb; ++ib) tile_ids.push_back(64 + (p.xb0 + k) * 8 + ib);
+    }
     const int T = static_cast<int>(tile_ids.size());
     CUtensorMap mv = make_map(V, ldv, n, w, p.tr);
     CUtensorMap mp = make_map(P, ldp, n, cp, p.tr);
@@ -653,7 +708,7 @@ void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 
     p.consumers = cw;
     const size_t red_bytes = static_cast<size_t>(cw) * T * 64 * 8;
     const size_t smem = std::max(ring_bytes(p), red_bytes) + 1024;
-    const void* fn = gram_fn<1, 1>(nbw, nb);
+    const void* fn = nx == 0 ? gram_fn<1, 1>(nbw, nb) : gram_x_fn<1>(nb, nx);
     if (!fn) fail(KRY_UNSUPPORTED, "gram shape");
     set_smem(fn, smem);
     void* args[] = {&mv, &mp, &p, &d_partials};

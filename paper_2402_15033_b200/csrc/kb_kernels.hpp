@@ -16,9 +16,12 @@ std::vector<std::pair<i64, i64>> prefix_groups(i64 c0, i64 w);
 i64 gram_scratch_doubles(i64 w);
 // Packed G tiles for one prefix group: tile_ids[t] = jb*8 + ib, 64 entries
 // per tile (8×8 column-major), written to d_packed in tile order.
+// x_first/x_count (optional, w ≤ 8 only): also return P[:,0:cp]ᵀ·P[:, x_first:x_first+x_count]
+// as extra tiles (ids 64 + xb*8 + ib, P-slot coordinates) — the panel Gram
+// pieces the two-stage finalize reuses (kb_store.cpp).
 void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V,
                       i64 ldv, i64 w, bool vv, double* d_partials, double* d_packed,
-                      std::vector<int>& tile_ids, int64_t& launches);
+                      std::vector<int>& tile_ids, int64_t& launches, i64 x_first = -1, i64 x_count = 0);
 int update_wmax(i64 w);
 // out = [V | P]·M on DMMA; d_mfrag holds M in fragment order (k_tsqr.cu, K5b).
 // Requires round_up(w,8) + round_up(cp,8) ≤ 64.

@@ -22,11 +22,14 @@ std::vector<std::pair<i64, i64>> groups_for(i64 c0, i64 w) {
 }  // namespace
 
 void gram_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
-                 Mat& r_col, Mat& g) {
+                 Mat& r_col, Mat& g, i64 x_first, i64 x_count, Mat* gx) {
     dim_check(w >= 1, "gram of empty matrix");
     const auto groups = groups_for(c0, w);
+    const bool want_x = gx && x_count > 0 && groups.size() == 1 && round_up(w, 8) == 8 && x_first >= 0 &&
+                        x_first + x_count <= c0;
+    if (gx) *gx = Mat();
     ctx.gram_partials.ensure(static_cast<size_t>(gram_scratch_doubles(w)) * 8);
-    ctx.gram_packed.ensure(groups.size() * 64 * 64 * 8);
+    ctx.gram_packed.ensure((groups.size() + 1) * 64 * 64 * 8);
     std::vector<std::vector<int>> tiles(groups.size());
 
     cudaEvent_t t0 = ctx.begin_phase();
@@ -34,7 +37,8 @@ void gram_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double
     for (size_t gi = 0; gi < groups.size(); ++gi) {
         const i64 start = groups[gi].first, cp = groups[gi].second;
         launch_gram_pass(ctx.stream, n, cp > 0 ? P + start * ldp : nullptr, ldp, cp, V, ldv, w, gi == 0,
-                         ctx.gram_partials.p, ctx.gram_packed.p + offset, tiles[gi], ctx.launches);
+                         ctx.gram_partials.p, ctx.gram_packed.p + offset, tiles[gi], ctx.launches,
+                         want_x ? x_first : -1, want_x ? x_count : 0);
         offset += tiles[gi].size() * 64;
     }
     ctx.end_phase(PH_GRAM, t0);
@@ -49,11 +53,21 @@ void gram_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double
     const i64 wslots = round_up(w, 8);
     r_col = Mat(c0, w);
     g = Mat(w, w);
+    if (want_x) *gx = Mat(c0, x_count);
     const double* h = ctx.h_packed.p;
     size_t off = 0;
     for (size_t gi = 0; gi < groups.size(); ++gi) {
         const i64 start = groups[gi].first, cp = groups[gi].second;
         for (int id : tiles[gi]) {
+            if (id >= 64) {  // extra P×P tile: rows slot block ib, columns slot block xb
+                const int xb = (id - 64) / 8, ib = (id - 64) % 8;
+                for (int e = 0; e < 64; ++e) {
+                    const i64 a = 8 * ib + (e & 7) - wslots, b = 8 * xb + (e >> 3) - wslots - x_first;
+                    if (a >= 0 && a < cp && b >= 0 && b < x_count) (*gx)(a, b) = h[off + e];
+                }
+                off += 64;
+                continue;
+            }
             const int jb = id / 8, ib = id % 8;
             for (int e = 0; e < 64; ++e) {
                 const i64 mrow = 8 * ib + (e & 7), j = 8 * jb + (e >> 3);
@@ -155,11 +169,18 @@ void update_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const doub
 }
 
 PipOut bcgs_pip_partial_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V,
-                               i64 ldv, i64 w, double* out, i64 ldo, i64& reduces, bool do_update) {
-    PipOut o;
+                               i64 ldv, i64 w, double* out, i64 ldo, i64& reduces, bool do_update, i64 x_first,
+                               i64 x_count, Mat* gx) {
     reduces += 1;  // fused [Q_prev, V]ᵀV (block_ortho.hpp:155)
-    Mat s;
-    gram_device(ctx, n, P, ldp, c0, V, ldv, w, o.r_col, s);
+    Mat r_col, s;
+    gram_device(ctx, n, P, ldp, c0, V, ldv, w, r_col, s, x_first, x_count, gx);
+    return pip_from_gram(ctx, n, P, ldp, c0, V, ldv, w, std::move(r_col), std::move(s), out, ldo, do_update);
+}
+
+PipOut pip_from_gram(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
+                     Mat r_col, Mat s, double* out, i64 ldo, bool do_update) {
+    PipOut o;
+    o.r_col = std::move(r_col);
     if (c0 > 0) {
         // Pythagorean update S = VᵀV − R_colᵀR_col, upper + mirror (block_ortho.hpp:159-166).
         for (i64 j = 0; j < w; ++j)

@@ -17,7 +17,14 @@ struct PipOut {
 // R_col = Pᵀ V (c0×w) and G = VᵀV (w×w, upper computed and mirrored, as
 // gram(), dense_kernels.hpp:95-105), summed over ranks.
 void gram_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
-                 Mat& r_col, Mat& g);
+                 Mat& r_col, Mat& g, i64 x_first = -1, i64 x_count = 0, Mat* gx = nullptr);
+// Optional extra output (first-stage shapes): gx = P[:, 0:c0]ᵀ·P[:, x_first:x_first+x_count]
+// (c0 × x_count), from the same launch and the same allreduce.
+
+// The part of bcgs_pip_partial after the Gram: Pythagorean update, Cholesky,
+// (update).  r_col / g as returned by gram_device.
+PipOut pip_from_gram(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
+                     Mat r_col, Mat g, double* out, i64 ldo, bool do_update);
 
 // out = (V − P·R_col)·R_jj⁻¹ (block_ortho.hpp:171-176 + tri_solve_right).
 void update_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
@@ -26,6 +33,7 @@ void update_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const doub
 // bcgs_pip_partial: adds 1 to `reduces`; writes the block to `out` only when
 // the Pythagorean Cholesky succeeds (bad_pivot == 0).
 PipOut bcgs_pip_partial_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V,
-                               i64 ldv, i64 w, double* out, i64 ldo, i64& reduces, bool do_update = true);
+                               i64 ldv, i64 w, double* out, i64 ldo, i64& reduces, bool do_update = true,
+                               i64 x_first = -1, i64 x_count = 0, Mat* gx = nullptr);
 
 }  // namespace kb

@@ -1,6 +1,7 @@
 #include "kb_store.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 
 #include "kb_ortho.hpp"
@@ -21,6 +22,9 @@ Store::Store(Ctx& ctx, i64 n, i64 m, i64 panel_size, i64 big_panel_size)
     if (big_panel_size_ % panel_size_ != 0 || big_panel_size_ > m)
         fail(KRY_DIMENSION_MISMATCH,
              "dimension mismatch: big panel size must be a multiple of the panel size, <= m");
+    pgram_ = Mat(max_cols_, max_cols_);
+    pready_.assign(static_cast<size_t>(max_cols_), 0);
+    if (const char* e = std::getenv("KRY_FUSED_PANEL_GRAM")) fused_panel_gram_ = std::atoi(e) != 0;
     q_.ensure(static_cast<size_t>(ld_) * max_cols_ * 8);
     KB_CUDA(cudaMemsetAsync(q_.p, 0, static_cast<size_t>(ld_) * max_cols_ * 8, ctx_.stream));
 }
@@ -50,6 +54,7 @@ bool Store::deferred_coefficients(const std::vector<double>& y, std::vector<doub
 
 void Store::reset() {
     pending_ = false;
+    std::fill(pready_.begin(), pready_.end(), 0);
     filled_ = 0;
     finalized_ = 0;
     big_panel_start_ = 0;
@@ -130,10 +135,18 @@ Outcome Store::append_impl(const double* V, i64 ldv, i64 w, bool overlap, int ki
 }
 
 Store::OrthoRes Store::pip(i64 c0, const double* V, i64 ldv, i64 w, double* out, i64 ldo, Sync& sync,
-                           bool first_pass, bool do_update) {
+                           bool first_pass, bool do_update, i64 x_first, i64 x_count) {
     i64 red = 0;
-    PipOut o = bcgs_pip_partial_device(ctx_, n_, col(0), ld_, c0, V, ldv, w, out, ldo, red, do_update);
+    Mat gx;
+    PipOut o = bcgs_pip_partial_device(ctx_, n_, col(0), ld_, c0, V, ldv, w, out, ldo, red, do_update, x_first,
+                                       x_count, x_count > 0 ? &gx : nullptr);
     sync.add(red);
+    if (gx.rows > 0) {  // panel Gram pieces for the previous block's (now final) columns
+        for (i64 b = 0; b < gx.cols; ++b) {
+            for (i64 a = 0; a < gx.rows; ++a) pgram_(a, x_first + b) = gx(a, b);
+            pready_[static_cast<size_t>(x_first + b)] = 1;
+        }
+    }
     // algorithmic bytes actually moved: Gram reads c0+w; the update reads c0+w and writes w
     ortho_bytes += do_update ? 8.0 * n_ * (2.0 * c0 + 3.0 * w) : 8.0 * n_ * (c0 + w);
     if (o.bad_pivot != 0) {
@@ -186,8 +199,25 @@ Mat project_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const doub
 
 Store::OrthoRes Store::run_scheme(i64 c0, const double* V, i64 ldv, i64 w, int kind, Sync& sync) {
     switch (kind) {
-        case KRY_ORTHO_TWO_STAGE:
-            return pip(c0, V, ldv, w, col(c0), ld_, sync, true);  // single first-stage pass
+        case KRY_ORTHO_TWO_STAGE: {  // single first-stage pass
+            // The previous block's columns are final now: let this Gram also
+            // produce their products with every earlier column (panel Gram).
+            // Only whole 8-column slot blocks are requested (one, at most two
+            // per Gram): a partial block costs a full block of DMMA work, and
+            // the extra tiles stay hidden under the HBM stream only while
+            // they are few.
+            i64 xf = -1, xc = 0;
+            if (fused_panel_gram_ && !records_.empty() && states_.back() == KRY_PANEL_PREPROCESSED) {
+                i64 xd = big_panel_start_;
+                while (xd < c0 && pready_[static_cast<size_t>(xd)]) ++xd;
+                const i64 xend = std::min(c0 / 8 * 8, xd / 8 * 8 + 16);
+                if (xend > xd) {
+                    xf = xd;
+                    xc = xend - xd;
+                }
+            }
+            return pip(c0, V, ldv, w, col(c0), ld_, sync, true, true, xf, xc);
+        }
         case KRY_ORTHO_BCGS_PIP2: {
             double* s0 = scratch(0, w);
             OrthoRes first = pip(c0, V, ldv, w, s0, ld_, sync, true);
@@ -305,7 +335,20 @@ Outcome Store::finalize_big_panel(Sync& sync, bool deferred) {
     const i64 w = filled_ - c0;
     OrthoRes res;
     try {
-        res = pip(c0, col(c0), ld_, w, col(c0), ld_, sync, true, /*do_update=*/!deferred);
+        Mat rc, g;
+        if (fused_finalize_gram(c0, w, rc, g)) {
+            sync.add(1);  // the last block's Gram: the panel's one reduce
+            PipOut o = pip_from_gram(ctx_, n_, col(0), ld_, c0, col(c0), ld_, w, std::move(rc), std::move(g),
+                                     col(c0), ld_, !deferred);
+            // Same algorithmic bytes as the unfused finalize:
+            // the Gram's reads of Q[:, 0:c_last) happened in the first stage.
+            ortho_bytes += !deferred ? 8.0 * n_ * (2.0 * c0 + 3.0 * w) : 8.0 * n_ * (c0 + w);
+            if (o.bad_pivot != 0) throw FirstPassFailure{o.bad_pivot};
+            res = OrthoRes{std::move(o.r_col), std::move(o.r_jj)};
+        } else {
+            res = pip(c0, col(c0), ld_, w, col(c0), ld_, sync, true, /*do_update=*/!deferred);
+        }
+        std::fill(pready_.begin() + c0, pready_.end(), 0);
         if (deferred) {
             pending_ = true;
             pend_c0_ = c0;
@@ -330,6 +373,41 @@ Outcome Store::finalize_big_panel(Sync& sync, bool deferred) {
     out.committed = w;
     sync.per_big_panel.push_back(sync.reduces - before);
     return out;
+}
+
+bool Store::fused_finalize_gram(i64 c0, i64 w, Mat& r_col, Mat& g) {
+    // The finalize Gram [Q_fin, P]ᵀP of the panel P = Q[:, c0:c0+w) from the
+    // pieces the first-stage Grams already produced (the panel's leading
+    // whole 8-column blocks) plus one narrow Gram of the trailing columns
+    // against everything before them: the same numbers, but a ≤16-wide Gram
+    // that streams at HBM speed instead of the compute-bound (w+1)-wide one.
+    // Falls back (false) when no piece is there.
+    if (!fused_panel_gram_) return false;
+    i64 c_last = c0;  // first panel column without its products
+    while (c_last < filled_ && pready_[static_cast<size_t>(c_last)]) ++c_last;
+    const i64 wl = filled_ - c_last;
+    if (c_last == c0 || wl < 1 || wl > 16) return false;
+    Mat rc2, g2;
+    gram_device(ctx_, n_, col(0), ld_, c_last, col(c_last), ld_, wl, rc2, g2);
+    r_col = Mat(c0, w);
+    g = Mat(w, w);
+    for (i64 j = 0; j < w; ++j) {
+        const i64 b = c0 + j;
+        if (b < c_last) {
+            for (i64 a = 0; a < c0; ++a) r_col(a, j) = pgram_(a, b);
+            for (i64 i = 0; i <= j; ++i) g(i, j) = pgram_(c0 + i, b);
+        } else {
+            const i64 jj = b - c_last;
+            for (i64 a = 0; a < c0; ++a) r_col(a, j) = rc2(a, jj);
+            for (i64 i = 0; i <= j; ++i) {
+                const i64 row = c0 + i;
+                g(i, j) = row < c_last ? rc2(row, jj) : g2(row - c_last, jj);
+            }
+        }
+    }
+    for (i64 j = 0; j < w; ++j)
+        for (i64 i = 0; i < j; ++i) g(j, i) = g(i, j);
+    return true;
 }
 
 void Store::combine_column(i64 c, i64 c0, i64 w, const OrthoRes& res) {

@@ -90,7 +90,13 @@ private:
     // Writes the orthonormal block into store columns [c0, c0+w).
     OrthoRes run_scheme(i64 c0, const double* V, i64 ldv, i64 w, int kind, Sync& sync);
     OrthoRes pip(i64 c0, const double* V, i64 ldv, i64 w, double* out, i64 ldo, Sync& sync, bool first_pass,
-                 bool do_update = true);
+                 bool do_update = true, i64 x_first = -1, i64 x_count = 0);
+    // Panel Gram pieces accumulated by the first-stage Grams (fused finalize):
+    // pgram_(a, b) = q_aᵀq_b for the preprocessed column b (pready_[b]) and a < b.
+    bool fused_panel_gram_ = true;
+    Mat pgram_;
+    std::vector<char> pready_;
+    bool fused_finalize_gram(i64 c0, i64 w, Mat& r_col, Mat& g);
     bool pending_ = false;  // deferred finalize transform below applies to Q[:, pend_c0_:pend_c0_+pend_w_)
     i64 pend_c0_ = 0, pend_w_ = 0;
     Mat pend_rcol_;

@@ -20,14 +20,16 @@
 //    streaming, see below), the order of
 //    bcgs_pip_partial's update + tri_solve_right (block_ortho.hpp:171-176,
 //    dense_kernels.hpp:139-154): vhat_j = V_j − Σ_l R_col(l,j)·p_l (l
-//    ascending), x_j = vhat_j − Σ_{l<j} R(l,j)·x_l, x_j *= 1/R(j,j).  One
-//    thread per row, coefficients broadcast from shared memory, output
-//    written coalesced (may alias V: in place over the basis store).
+//    ascending), x_j = vhat_j − Σ_{l<j} R(l,j)·x_l, x_j *= 1/R(j,j).  Two
+//    adjacent rows per thread (16-byte loads), coefficients broadcast from
+//    shared memory, output written coalesced (may alias V: in place over the
+//    basis store).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 #include <unordered_map>
@@ -326,8 +328,8 @@ const void* gram_x_fn(int nb, int nx) {
 }
 
 // ---------------------------------------------------------------------------
-// K5: fused update  out = (V − P·R_col)·R_jj⁻¹, one thread per row, in place
-// over the store (out may alias V; P never aliases out).  Coalesced 256-byte
+// K5: fused update  out = (V − P·R_col)·R_jj⁻¹, row-local (R rows per thread), in place
+// over the store (out may alias V; P never aliases out).  Coalesced 512-byte
 // warp loads/stores straight from HBM at high occupancy; the coefficients are
 // broadcast from shared memory.  Both loops are right-looking so every row
 // keeps w independent FMA chains, while each element still receives its
@@ -335,7 +337,129 @@ const void* gram_x_fn(int nb, int nx) {
 // coef layout (doubles): nrc[cp][WMAX] = −R_col, nrjj[WMAX][WMAX] = −R_jj(l,j)
 // for l < j, inv[WMAX] = 1/R_jj(j,j).
 // ---------------------------------------------------------------------------
-template <int WMAX>
+// R rows per thread (R = 2: 16-byte loads/stores of two adjacent rows —
+// half the load instructions and coefficient broadcasts per element).
+template <int R>
+struct RowVec;
+template <>
+struct RowVec<1> {
+    static __device__ __forceinline__ void ld(const double* p, double (&d)[1]) { d[0] = __ldg(p); }
+    static __device__ __forceinline__ void ldv(const double* p, double (&d)[1]) { d[0] = *p; }
+    static __device__ __forceinline__ void st(double* p, const double (&d)[1]) { *p = d[0]; }
+};
+template <>
+struct RowVec<2> {
+    static __device__ __forceinline__ void ld(const double* p, double (&d)[2]) {
+        const double2 t = __ldg(reinterpret_cast<const double2*>(p));
+        d[0] = t.x;
+        d[1] = t.y;
+    }
+    static __device__ __forceinline__ void ldv(const double* p, double (&d)[2]) {
+        const double2 t = *reinterpret_cast<const double2*>(p);
+        d[0] = t.x;
+        d[1] = t.y;
+    }
+    static __device__ __forceinline__ void st(double* p, const double (&d)[2]) {
+        *reinterpret_cast<double2*>(p) = make_double2(d[0], d[1]);
+    }
+};
+
+// Rows [row, row + R) of the update (every row computed in exactly the
+// scalar order, so R = 1 and R = 2 give identical bits).
+template <int WMAX, int R>
+__device__ __forceinline__ void update_rows(i64 row, const double* __restrict__ P, i64 ldp, int cp, int cpp,
+                                            const double* V, i64 ldv, int w, const double* nrc,
+                                            const double* nrjj, const double* inv, int triangular, double* out,
+                                            i64 ldo) {
+    using RV = RowVec<R>;
+    double acc[WMAX][R];
+#pragma unroll
+    for (int j = 0; j < WMAX; ++j) {
+        if (j < w) {
+            RV::ldv(V + row + j * ldv, acc[j]);
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[j][r] = 0.0;
+        }
+    }
+    // Prefix columns in batches of 4 through a 3-deep register ring: two
+    // batches are in flight while one is consumed.  The coefficient rows are
+    // zero-padded to a multiple of 12 (see the shared-memory fill), so there
+    // is no tail loop; loads past cp are predicated off.
+    const double* prow = P + row;
+    const int nb = cpp / 4;
+    double b0[4][R], b1[4][R], b2[4][R];
+    auto ld = [&](double (&dst)[4][R], int bt) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const int l = 4 * bt + u;
+            if (l < cp) {
+                RV::ld(prow + static_cast<i64>(l) * ldp, dst[u]);
+            } else {
+#pragma unroll
+                for (int r = 0; r < R; ++r) dst[u][r] = 0.0;
+            }
+        }
+    };
+    auto fm = [&](const double (&src)[4][R], int bt) {
+#pragma unroll
+        for (int u = 0; u < 4; ++u) {
+            const double2* cr = reinterpret_cast<const double2*>(nrc + (4 * bt + u) * WMAX);
+#pragma unroll
+            for (int j = 0; j < WMAX; j += 2) {
+                const double2 c = cr[j / 2];
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    acc[j][r] = fma(c.x, src[u][r], acc[j][r]);
+                    acc[j + 1][r] = fma(c.y, src[u][r], acc[j + 1][r]);
+                }
+            }
+        }
+    };
+    if (nb > 0) {
+        ld(b0, 0);
+        ld(b1, 1);
+    }
+    for (int bt = 0; bt < nb; bt += 3) {  // nb is a multiple of 3
+        ld(b2, bt + 2);
+        fm(b0, bt);
+        ld(b0, bt + 3);
+        fm(b1, bt + 1);
+        ld(b1, bt + 4);
+        fm(b2, bt + 2);
+    }
+    if (triangular) {
+        // Right-looking substitution: acc_j receives −R(k,j)·x_k for
+        // k = 0, 1, … in order, then ×1/R(j,j) — tri_solve_right's order.
+#pragma unroll
+        for (int k = 0; k < WMAX; ++k) {
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[k][r] *= inv[k];
+            const double* rk = nrjj + k * WMAX;
+            if ((k + 1) & 1) {  // odd first column: one scalar step to reach a pair boundary
+                if (k + 1 < WMAX)
+#pragma unroll
+                    for (int r = 0; r < R; ++r) acc[k + 1][r] = fma(rk[k + 1], acc[k][r], acc[k + 1][r]);
+            }
+#pragma unroll
+            for (int j = (k + 2) & ~1; j < WMAX; j += 2) {
+                const double2 c = *reinterpret_cast<const double2*>(rk + j);
+#pragma unroll
+                for (int r = 0; r < R; ++r) {
+                    acc[j][r] = fma(c.x, acc[k][r], acc[j][r]);
+                    acc[j + 1][r] = fma(c.y, acc[k][r], acc[j + 1][r]);
+                }
+            }
+        }
+    }
+#pragma unroll
+    for (int j = 0; j < WMAX; ++j)
+        if (j < w) RV::st(out + row + j * ldo, acc[j]);
+}
+
+// R = 2 requires even ld's and 16-byte aligned P/V/out (the store's layout);
+// an odd last row is finished by the scalar path.
+template <int WMAX, int R>
 __global__ void __launch_bounds__(256)
     update_kernel(i64 n, const double* __restrict__ P, i64 ldp, int cp, const double* V, i64 ldv, int w,
                   const double* __restrict__ coef, int triangular, double* out, i64 ldo) {
@@ -352,72 +476,12 @@ __global__ void __launch_bounds__(256)
     const double* nrc = c_sm;
     const double* nrjj = c_sm + static_cast<size_t>(cpp) * WMAX;
     const double* inv = nrjj + WMAX * WMAX;
-    for (i64 row = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x; row < n;
-         row += static_cast<i64>(gridDim.x) * blockDim.x) {
-        double acc[WMAX];
-#pragma unroll
-        for (int j = 0; j < WMAX; ++j) acc[j] = (j < w) ? V[row + j * ldv] : 0.0;
-        // Prefix columns in batches of 4 through a 3-deep register ring: two
-        // batches (8 loads) are in flight while one is consumed.  The
-        // coefficient rows are zero-padded to a multiple of 12 (see the
-        // shared-memory fill), so there is no tail loop; loads past cp are
-        // predicated off.
-        const double* prow = P + row;
-        const int nb = cpp / 4;
-        double b0[4], b1[4], b2[4];
-        auto ld = [&](double (&dst)[4], int bt) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int l = 4 * bt + u;
-                dst[u] = l < cp ? __ldg(prow + static_cast<i64>(l) * ldp) : 0.0;
-            }
-        };
-        auto fm = [&](const double (&src)[4], int bt) {
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const double2* cr = reinterpret_cast<const double2*>(nrc + (4 * bt + u) * WMAX);
-#pragma unroll
-                for (int j = 0; j < WMAX; j += 2) {
-                    const double2 c = cr[j / 2];
-                    acc[j] = fma(c.x, src[u], acc[j]);
-                    acc[j + 1] = fma(c.y, src[u], acc[j + 1]);
-                }
-            }
-        };
-        if (nb > 0) {
-            ld(b0, 0);
-            ld(b1, 1);
-        }
-        for (int bt = 0; bt < nb; bt += 3) {  // nb is a multiple of 3
-            ld(b2, bt + 2);
-            fm(b0, bt);
-            ld(b0, bt + 3);
-            fm(b1, bt + 1);
-            ld(b1, bt + 4);
-            fm(b2, bt + 2);
-        }
-        if (triangular) {
-            // Right-looking substitution: acc_j receives −R(k,j)·x_k for
-            // k = 0, 1, … in order, then ×1/R(j,j) — tri_solve_right's order.
-#pragma unroll
-            for (int k = 0; k < WMAX; ++k) {
-                acc[k] *= inv[k];
-                const double* rk = nrjj + k * WMAX;
-                if ((k + 1) & 1) {  // odd first column: one scalar step to reach a pair boundary
-                    if (k + 1 < WMAX) acc[k + 1] = fma(rk[k + 1], acc[k], acc[k + 1]);
-                }
-#pragma unroll
-                for (int j = (k + 2) & ~1; j < WMAX; j += 2) {
-                    const double2 c = *reinterpret_cast<const double2*>(rk + j);
-                    acc[j] = fma(c.x, acc[k], acc[j]);
-                    acc[j + 1] = fma(c.y, acc[k], acc[j + 1]);
-                }
-            }
-        }
-#pragma unroll
-        for (int j = 0; j < WMAX; ++j)
-            if (j < w) out[row + j * ldo] = acc[j];
-    }
+    const i64 groups = n / R;
+    const i64 tid = blockIdx.x * static_cast<i64>(blockDim.x) + threadIdx.x;
+    for (i64 g = tid; g < groups; g += static_cast<i64>(gridDim.x) * blockDim.x)
+        update_rows<WMAX, R>(g * R, P, ldp, cp, cpp, V, ldv, w, nrc, nrjj, inv, triangular, out, ldo);
+    if (R > 1 && tid < n - groups * R)
+        update_rows<WMAX, 1>(groups * R + tid, P, ldp, cp, cpp, V, ldv, w, nrc, nrjj, inv, triangular, out, ldo);
 }
 
 // Wide blocks (33 ≤ w ≤ 64, the ŝ+1 finalize panel): two threads per row.
@@ -742,6 +806,15 @@ void launch_update_mma(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64
     launches += 1;
 }
 
+static int update_rows_setting() {  // KRY_UPDATE_ROWS=1 → one row per thread (A/B)
+    static const int r = [] {
+        const char* e = std::getenv("KRY_UPDATE_ROWS");
+        const int v = e ? std::atoi(e) : 2;
+        return v == 1 ? 1 : 2;
+    }();
+    return r;
+}
+
 int update_wmax(i64 w) { return w <= 6 ? 6 : w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64; }
 
 void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
@@ -749,20 +822,26 @@ void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp,
     const int wmax = update_wmax(w);
     const size_t smem = static_cast<size_t>(round_up(cp, 12) + wmax + 1) * wmax * 8;
     if (smem > 200 * 1024) fail(KRY_UNSUPPORTED, "update coefficients exceed shared memory");
+    // Two rows per thread when the layout allows 16-byte accesses.
+    const int rsel = update_rows_setting();
+    const bool vec = wmax <= 16 && rsel > 1 && ((ldp | ldv | ldo) & 1) == 0 &&
+                     ((reinterpret_cast<uintptr_t>(P) | reinterpret_cast<uintptr_t>(V) |
+                       reinterpret_cast<uintptr_t>(out)) & 15) == 0;
+    const i64 rows_per_thread = vec ? 2 : 1;
     auto go = [&](auto kernel) {
         set_smem(reinterpret_cast<const void*>(kernel), smem);
         int per_sm = 0;
         KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem));
-        const i64 want = ceil_div(n, wmax == 64 ? 128 : 256);
+        const i64 want = ceil_div(n, (wmax == 64 ? 128 : 256) * rows_per_thread);
         const int grid = static_cast<int>(std::max<i64>(1, std::min<i64>(want, static_cast<i64>(sm_count()) * std::max(per_sm, 1))));
         kernel<<<grid, 256, smem, stream>>>(n, P, ldp, static_cast<int>(cp), V, ldv, static_cast<int>(w), d_coef,
                                             triangular ? 1 : 0, out, ldo);
     };
     switch (wmax) {
-        case 6: go(update_kernel<6>); break;
-        case 8: go(update_kernel<8>); break;
-        case 16: go(update_kernel<16>); break;
-        case 32: go(update_kernel<32>); break;
+        case 6: vec ? go(update_kernel<6, 2>) : go(update_kernel<6, 1>); break;
+        case 8: vec ? go(update_kernel<8, 2>) : go(update_kernel<8, 1>); break;
+        case 16: vec ? go(update_kernel<16, 2>) : go(update_kernel<16, 1>); break;
+        case 32: go(update_kernel<32, 1>); break;
         default: go(update_pair_kernel); break;  // coefficients in the interleaved layout
     }
     KB_LAUNCHED();

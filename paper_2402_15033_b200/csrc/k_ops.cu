@@ -14,7 +14,9 @@
 // reproducible run to run (no float atomics).
 #include <cuda_runtime.h>
 
+#include <algorithm>
 #include <mutex>
+#include <type_traits>
 
 #include "kb_common.hpp"
 #include "kb_kernels.hpp"
@@ -215,6 +217,130 @@ __global__ void __launch_bounds__(kBlock) stencil2d_vec_kernel(const StencilGeom
     }
 }
 
+// K2f: the whole s-step MPK of the 5-point stencil in one pass
+// (mpk_monomial, gmres.hpp:80-90): out[:, k−1] = A^k·x for k = 1..S.
+// Temporal blocking: each warp owns a 64-column window (32 lanes × double2)
+// and a band of grid lines, and streams the band's input lines once, bottom
+// to top.  Level k runs 2k − 1 lines behind the input (skewed wavefront):
+// at step t it produces line L − 2k + 1 from lines of level k − 1 finished in
+// the three previous steps, so the S levels of one step are independent
+// (ILP instead of an S-deep dependency chain).  Each level keeps its last
+// three lines in a register ring indexed by t mod 3, and the input lines
+// are prefetched three steps ahead in a second ring; the step loop is
+// unrolled by 3 so no ring ever moves.  Horizontal neighbours come by
+// shuffle.  Level k is valid on the window shrunk by k columns per side, so
+// a window outputs its middle 64 − 2H columns (H = S rounded up to even)
+// and neighbouring windows overlap by 2H; bands start S lines early
+// (recomputed, never stored).  HBM traffic per MPK: one read of x (+ the
+// overlaps, mostly L2) and S writes, versus S reads and S writes for S
+// separate SpMVs.
+//
+// Bit-identity with spmv (csr_matrix.hpp:72-77): every element is
+// 0.0 + t_0 + t_1 + … in stored column order with t = −x (exact, so one
+// add of the negated value) or 4·x.  Absent neighbours (grid edges) are
+// carried as +0.0 and added as −0.0: a running sum that starts at +0.0 can
+// never be −0.0 under round-to-nearest, so s + (−0.0) = s bit for bit — the
+// same result as skipping the term.
+constexpr int kMpkRing = 3;
+
+template <int S>
+__device__ __forceinline__ void mpk2d_task(const StencilGeom& g, const double* __restrict__ x,
+                                           const double* __restrict__ halo_lo, const double* __restrict__ halo_hi,
+                                           double* __restrict__ out, i64 ldo, int wb, int wx, int band, int lane) {
+    constexpr int H = (S + 1) & ~1;
+    constexpr int STEP = 64 - 2 * H;
+    // 32-bit line/column arithmetic (grid dimensions < 2^31; checked by
+    // mpk2d_supported), 64-bit only in addresses.
+    const int nx = static_cast<int>(g.nx), ny = static_cast<int>(g.ny);
+    const int lines = static_cast<int>(g.lines), line0 = static_cast<int>(g.line0);
+    const int ix = wx * STEP - H + 2 * lane;  // this lane's first column (even)
+    const bool in_grid = ix >= 0 && ix < nx;  // nx even: both columns or neither
+    const bool store_lane = in_grid && lane >= H / 2 && lane < 32 - H / 2;
+    const int y0 = wb * band, y1 = min(y0 + band, lines);
+    // Input lines from ls: S below the band (or from the grid's first line);
+    // level S reaches line y1 − 1 at step y1 + 2S − 2 − ls.
+    const int ls = max(y0 - S, -line0);
+    const int steps = y1 + 2 * S - 1 - ls;
+    const int lmax = min(lines + S, ny - line0);  // first line with no data (zeros above)
+    const i64 nx64 = nx;
+    auto load = [&](int l) -> double2 {
+        double2 v = make_double2(0.0, 0.0);
+        if (in_grid && l < lmax) {
+            const double* p = l < 0        ? halo_lo + static_cast<i64>(l + S) * nx64
+                              : l < lines ? x + static_cast<i64>(l) * nx64
+                                          : halo_hi + static_cast<i64>(l - lines) * nx64;
+            v = __ldg(reinterpret_cast<const double2*>(p + ix));
+        }
+        return v;
+    };
+    // r[t mod 3][j]: level j's line finished at step t (level 0: input line).
+    double2 r[kMpkRing][S];
+#pragma unroll
+    for (int q = 0; q < kMpkRing; ++q)
+#pragma unroll
+        for (int j = 0; j < S; ++j) r[q][j] = make_double2(0.0, 0.0);
+    double2 pf[kMpkRing];  // input lines of steps t, t+1, t+2
+#pragma unroll
+    for (int q = 0; q < kMpkRing; ++q) pf[q] = load(ls + q);
+    double* const out_ix = out + ix;
+    auto step = [&](auto phase, int st) {
+        constexpr int P = decltype(phase)::value;  // st ≡ P (mod 3)
+        constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3, P3 = P;  // steps t−1, t−2, t−3
+        const int L = ls + st;
+        const double2 in = pf[P];
+        pf[P] = load(L + kMpkRing);
+        double* const orow = out_ix + static_cast<i64>(L) * nx64;
+        // Top level first: level k reads the old lines of level k − 1
+        // (slot P3 holds step t − 3 until level k − 1 overwrites it below).
+#pragma unroll
+        for (int k = S; k >= 1; --k) {
+            const int l = L - 2 * k + 1;  // level k's line this step
+            const int gl = line0 + l;
+            const double2 dn = k == 1 ? r[P2][0] : r[P3][k - 1];
+            const double2 cu = k == 1 ? r[P1][0] : r[P2][k - 1];
+            const double2 up = k == 1 ? in : r[P1][k - 1];
+            const double left = __shfl_up_sync(0xffffffffu, cu.y, 1);
+            const double right = __shfl_down_sync(0xffffffffu, cu.x, 1);
+            double s0 = __dadd_rn(0.0, -dn.x);
+            s0 = __dadd_rn(s0, -left);
+            s0 = acc_term(s0, 4.0, cu.x);
+            s0 = __dadd_rn(s0, -cu.y);
+            s0 = __dadd_rn(s0, -up.x);
+            double s1 = __dadd_rn(0.0, -dn.y);
+            s1 = __dadd_rn(s1, -cu.x);
+            s1 = acc_term(s1, 4.0, cu.y);
+            s1 = __dadd_rn(s1, -right);
+            s1 = __dadd_rn(s1, -up.y);
+            // outside the grid (lines or columns): exactly +0.0
+            const bool live = in_grid && gl >= 0 && gl < ny;
+            const double2 v = live ? make_double2(s0, s1) : make_double2(0.0, 0.0);
+            if (store_lane && l >= y0 && l < y1)
+                *reinterpret_cast<double2*>(orow + ((k - 1) * ldo - (2 * k - 1) * nx64)) = v;
+            if (k < S) r[P][k] = v;
+        }
+        r[P][0] = in;
+    };
+    for (int st = 0; st < steps; st += kMpkRing) {  // steps past the end are harmless (nothing stored)
+        step(std::integral_constant<int, 0>{}, st);
+        step(std::integral_constant<int, 1>{}, st + 1);
+        step(std::integral_constant<int, 2>{}, st + 2);
+    }
+}
+
+template <int S>
+__global__ void __launch_bounds__(kBlock, 2) mpk2d_kernel(const StencilGeom g, const double* __restrict__ x,
+                                                       const double* __restrict__ halo_lo,
+                                                       const double* __restrict__ halo_hi,
+                                                       double* __restrict__ out, i64 ldo, i64 nwx, i64 band,
+                                                       i64 ntasks) {
+    const int lane = threadIdx.x & 31;
+    const i64 nwarps = static_cast<i64>(gridDim.x) * (kBlock / 32);
+    for (i64 task = blockIdx.x * static_cast<i64>(kBlock / 32) + (threadIdx.x >> 5); task < ntasks;
+         task += nwarps)  // whole warps only
+        mpk2d_task<S>(g, x, halo_lo, halo_hi, out, ldo, static_cast<int>(task / nwx), static_cast<int>(task % nwx),
+                      static_cast<int>(band), lane);
+}
+
 // CSR SpMV, one warp per 32 consecutive rows: the warp's contiguous nnz range
 // (values + int32 columns) is staged through shared memory with coalesced
 // loads in chunks of kCsrChunk entries, then each lane sums its own row
@@ -393,6 +519,45 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
     KB_LAUNCHED();
     ++launches;
     return b ? static_cast<int>(grid.x * grid.y) : 0;
+}
+
+bool mpk2d_supported(const StencilGeom& g, int s, const double* x, const double* out, i64 ldo) {
+    auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    return g.dims == 2 && (g.nx & 1) == 0 && s >= 1 && s <= 8 && (ldo & 1) == 0 && a16(x) && a16(out) &&
+           g.lines >= 1 && g.nx + 64 < (i64(1) << 31) && g.ny + 64 < (i64(1) << 31);
+}
+
+void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const double* halo_lo,
+                  const double* halo_hi, double* out, i64 ldo, int s, int64_t& launches) {
+    const int h = (s + 1) & ~1, step = 64 - 2 * h;
+    const i64 nwx = ceil_div(g.nx, step);
+    auto go = [&](auto kernel) {
+        // One wave of resident warps, one (window, band) task each: bands as
+        // tall as that allows (the 2s-line band overlap is recomputed), at
+        // least 4s lines; very wide grids loop over tasks.
+        int per_sm = 0;
+        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+        const i64 resident = static_cast<i64>(num_sms()) * std::max(per_sm, 1) * (kBlock / 32);
+        const i64 nbands = std::max<i64>(1, std::min<i64>(resident / nwx, g.lines / (4 * s)));
+        const i64 band = ceil_div(g.lines, nbands);
+        const i64 ntasks = nwx * ceil_div(g.lines, band);
+        const unsigned grid = static_cast<unsigned>(
+            std::min<i64>(ceil_div(ntasks, kBlock / 32), static_cast<i64>(num_sms()) * std::max(per_sm, 1)));
+        kernel<<<grid, kBlock, 0, st>>>(g, x, halo_lo, halo_hi, out, ldo, nwx, band, ntasks);
+    };
+    switch (s) {
+        case 1: go(mpk2d_kernel<1>); break;
+        case 2: go(mpk2d_kernel<2>); break;
+        case 3: go(mpk2d_kernel<3>); break;
+        case 4: go(mpk2d_kernel<4>); break;
+        case 5: go(mpk2d_kernel<5>); break;
+        case 6: go(mpk2d_kernel<6>); break;
+        case 7: go(mpk2d_kernel<7>); break;
+        case 8: go(mpk2d_kernel<8>); break;
+        default: fail(KRY_INTERNAL, "mpk2d: unsupported s");
+    }
+    KB_LAUNCHED();
+    ++launches;
 }
 
 int launch_csr(cudaStream_t s, i64 nloc, const int64_t* row_ptr, const int32_t* col, const double* vals,

@@ -370,7 +370,8 @@ int kry_mpk(kry_ctx* ctx, kry_operator* op, const double* start, int64_t s, doub
         const i64 n = op->op->nloc, ld = kb::device_ld(n);
         ctx->up0.ensure(mat_bytes(ld, s + 1));
         KB_CUDA(cudaMemcpyAsync(ctx->up0.p, start, static_cast<size_t>(n) * 8, cudaMemcpyHostToDevice, c.stream));
-        for (i64 k = 0; k < s; ++k) op->op->apply(ctx->up0.p + k * ld, ctx->up0.p + (k + 1) * ld);
+        if (s == 0 || !op->op->mpk(ctx->up0.p, ctx->up0.p + ld, ld, static_cast<int>(s)))
+            for (i64 k = 0; k < s; ++k) op->op->apply(ctx->up0.p + k * ld, ctx->up0.p + (k + 1) * ld);
         download(c, v, ctx->up0.p, ld, n, s + 1);
         c.sync();
     });

@@ -50,6 +50,11 @@ StencilGeom make_stencil_geom(int dims, i64 nx, i64 ny, i64 nz, i64 row_begin, i
 int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const double* halo_lo,
                    const double* halo_hi, const double* b, double* y, double* partials, int64_t& launches);
 int stencil_partials(const StencilGeom& g);
+// Fused 2-D MPK: out[:, k−1] = A^k·x, k = 1..s (out columns ldo apart), one
+// pass; halos hold s lines each (multi-rank).
+bool mpk2d_supported(const StencilGeom& g, int s, const double* x, const double* out, i64 ldo);
+void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const double* halo_lo,
+                  const double* halo_hi, double* out, i64 ldo, int s, int64_t& launches);
 // CSR rows (row_ptr local, from 0) gathering x through int32 indices.
 int launch_csr(cudaStream_t s, i64 nloc, const int64_t* row_ptr, const int32_t* col, const double* vals,
                const double* x, const double* b, double* y, double* partials, int64_t& launches);

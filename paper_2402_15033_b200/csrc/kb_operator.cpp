@@ -1,6 +1,7 @@
 #include "kb_operator.hpp"
 
 #include <algorithm>
+#include <cstdlib>
 #include <limits>
 #include <vector>
 
@@ -157,6 +158,35 @@ int Operator::apply(const double* x, double* y, const double* b) {
         KB_NCCL(ncclGroupEnd());
     }
     return launch_stencil(c.stream, geom, x, halo_lo.p, halo_hi.p, b, y, part, c.launches);
+}
+
+bool Operator::mpk(const double* x, double* out, i64 ldo, int s) {
+    static const bool enabled = [] {
+        const char* e = std::getenv("KRY_FUSED_MPK");
+        return !e || std::atoi(e) != 0;
+    }();
+    Ctx& c = *ctx;
+    // Every rank must own at least s lines (the halo is the neighbour's s
+    // edge lines); the partition differs by at most one line between ranks.
+    if (!enabled || kind != LAPLACE2D || geom.ny / c.nranks < s || !mpk2d_supported(geom, s, x, out, ldo))
+        return false;
+    const i64 h = static_cast<i64>(s) * geom.nx;
+    if (c.nranks > 1) {
+        mpk_lo.ensure(static_cast<size_t>(h) * 8);
+        mpk_hi.ensure(static_cast<size_t>(h) * 8);
+        KB_NCCL(ncclGroupStart());
+        if (c.rank > 0) {
+            KB_NCCL(ncclSend(x, static_cast<size_t>(h), ncclDouble, c.rank - 1, c.comm, c.stream));
+            KB_NCCL(ncclRecv(mpk_lo.p, static_cast<size_t>(h), ncclDouble, c.rank - 1, c.comm, c.stream));
+        }
+        if (c.rank + 1 < c.nranks) {
+            KB_NCCL(ncclSend(x + nloc - h, static_cast<size_t>(h), ncclDouble, c.rank + 1, c.comm, c.stream));
+            KB_NCCL(ncclRecv(mpk_hi.p, static_cast<size_t>(h), ncclDouble, c.rank + 1, c.comm, c.stream));
+        }
+        KB_NCCL(ncclGroupEnd());
+    }
+    launch_mpk2d(c.stream, geom, x, mpk_lo.p, mpk_hi.p, out, ldo, s, c.launches);
+    return true;
 }
 
 double Operator::bytes_per_apply() const {

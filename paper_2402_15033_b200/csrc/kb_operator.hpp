@@ -26,6 +26,11 @@ struct Operator {
     // y = A·x (b == nullptr) or y = b − A·x with Σy² partials in `partials`;
     // returns the number of partials written (0 without b).
     int apply(const double* x, double* y, const double* b = nullptr);
+    // The whole monomial MPK out[:, k−1] = A^k·x, k = 1..s, in one fused
+    // pass when the operator supports it (2-D stencil); false otherwise
+    // (the caller then applies s times).  Collective over the ranks.
+    bool mpk(const double* x, double* out, i64 ldo, int s);
+    DevBuf mpk_lo, mpk_hi;    // s-line halos of the fused MPK
     // bytes moved by one application (algorithmic)
     double bytes_per_apply() const;
 };

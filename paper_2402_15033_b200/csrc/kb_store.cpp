@@ -84,6 +84,7 @@ double* Store::scratch(int which, i64 w) {
 
 void Store::mpk(Operator& op, i64 c0, i64 s) {
     dim_check(c0 + s + 1 <= max_cols_, "basis store capacity exceeded");
+    if (op.mpk(col(c0), col(c0 + 1), ld_, static_cast<int>(s))) return;
     for (i64 k = 0; k < s; ++k) op.apply(col(c0 + k), col(c0 + k + 1));
 }
 

@@ -75,6 +75,21 @@ def test_mpk_bitwise(kb, ctx, ref, rng, s):
     np.testing.assert_array_equal(op.mpk(start, s), ref.mpk(a, start, s))
 
 
+# The fused 2-D MPK (one pass, temporal blocking; k_ops.cu mpk2d_kernel):
+# window seams (nx > 52), band seams (ny > 4s), odd nx (per-SpMV fallback),
+# s up to 8, grids narrower than one window.
+@pytest.mark.parametrize("nx,ny,s", [(130, 97, 5), (200, 64, 8), (52, 200, 2), (8, 300, 7), (131, 50, 5),
+                                     (106, 41, 1), (64, 9, 6), (2, 2, 3),
+                                     # a window's last lane on the grid's last column
+                                     (110, 40, 5), (58, 30, 6), (104, 50, 8), (60, 33, 3), (62, 20, 1)])
+def test_mpk_fused_bitwise(kb, ctx, ref, rng, nx, ny, s):
+    a = ref.laplace2d(nx, ny)
+    op = kb.Laplace2D(nx, ny)
+    start = rng.standard_normal(a.n)
+    start /= np.linalg.norm(start)
+    np.testing.assert_array_equal(op.mpk(start, s), ref.mpk(a, start, s))
+
+
 def test_spmv_rejects_bad_length(kb, ctx):
     op = kb.Laplace2D(4, 4)
     with pytest.raises(kb.DimensionMismatch):

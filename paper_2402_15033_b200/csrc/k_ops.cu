@@ -341,46 +341,68 @@ __global__ void __launch_bounds__(kBlock, 2) mpk2d_kernel(const StencilGeom g, c
                       static_cast<int>(band), lane);
 }
 
-// CSR SpMV, one warp per 32 consecutive rows: the warp's contiguous nnz range
-// (values + int32 columns) is staged through shared memory with coalesced
-// loads in chunks of kCsrChunk entries, then each lane sums its own row
-// sequentially in stored order (bit-identical to spmv, csr_matrix.hpp:72-77)
-// — rows of ~30 entries no longer make every lane stride through memory.
+// CSR SpMV, one warp per 32 consecutive rows, in two phases per chunk of
+// the warp's contiguous nnz range (kCsrChunk entries):
+//  1. gather — lanes stride over the chunk's entries (coalesced val / col
+//     loads, streamed past L2 with evict-first so x keeps the cache) and form
+//     the products val·x[col]; all kCsrChunk/32 gathers of a lane are issued
+//     before any is used, so the random x reads overlap instead of
+//     serialising behind each row's running sum;
+//  2. sum — each lane adds its own row's products from shared memory in
+//     stored order.
+// The product is the same rounded __dmul_rn as in the sequential loop and
+// the adds keep spmv's order (csr_matrix.hpp:72-77): bit-identical.
 constexpr int kCsrChunk = 256;
 
-template <bool RESID>
-__global__ void __launch_bounds__(kBlock) csr_warp_kernel(i64 nloc, const int64_t* __restrict__ row_ptr,
+// MODE: CSR_ONLY (s from 0.0, write y), or one pass of a column-sliced SpMV
+// (see Operator in kb_operator.cpp): CSR_FIRST (s from 0.0, write the
+// partial), CSR_MID (partial in/out), CSR_LAST (partial in, write y).
+enum CsrMode { CSR_ONLY = 0, CSR_FIRST = 1, CSR_MID = 2, CSR_LAST = 3 };
+
+template <int MODE, bool RESID, typename RP>
+__global__ void __launch_bounds__(kBlock) csr_warp_kernel(i64 nloc, const RP* __restrict__ row_ptr,
                                                           const int32_t* __restrict__ col,
                                                           const double* __restrict__ vals,
                                                           const double* __restrict__ x,
                                                           const double* __restrict__ b, double* __restrict__ y,
-                                                          double* __restrict__ partials) {
-    __shared__ double s_val[kBlock / 32][kCsrChunk];
-    __shared__ int32_t s_col[kBlock / 32][kCsrChunk];
+                                                          double* __restrict__ partials, double* part_sum) {
+    __shared__ double s_prod[kBlock / 32][kCsrChunk];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const i64 stride = static_cast<i64>(gridDim.x) * (kBlock / 32) * 32;
     double sq = 0.0;
     for (i64 r0 = (static_cast<i64>(blockIdx.x) * (kBlock / 32) + warp) * 32; r0 < nloc; r0 += stride) {
         const i64 row = r0 + lane;
         const bool live = row < nloc;
-        const i64 rs = live ? row_ptr[row] : 0, re = live ? row_ptr[row + 1] : 0;
+        const i64 rs = live ? static_cast<i64>(row_ptr[row]) : 0, re = live ? static_cast<i64>(row_ptr[row + 1]) : 0;
         const i64 last = (nloc - 1 - r0) < 31 ? (nloc - 1 - r0) : 31;
         const i64 base = __shfl_sync(0xffffffffu, rs, 0);
         const i64 end = __shfl_sync(0xffffffffu, re, static_cast<int>(last));
         double s = 0.0;
+        if ((MODE == CSR_MID || MODE == CSR_LAST) && live) s = part_sum[row];
         for (i64 cs = base; cs < end; cs += kCsrChunk) {
             const int cnt = static_cast<int>((end - cs) < kCsrChunk ? (end - cs) : kCsrChunk);
-            for (int k = lane; k < cnt; k += 32) {
-                s_val[warp][k] = vals[cs + k];
-                s_col[warp][k] = col[cs + k];
+            int cidx[kCsrChunk / 32];
+            double v[kCsrChunk / 32];
+#pragma unroll
+            for (int u = 0; u < kCsrChunk / 32; ++u) {
+                const int k = lane + 32 * u;
+                cidx[u] = k < cnt ? __ldcs(col + cs + k) : 0;
+                v[u] = k < cnt ? __ldcs(vals + cs + k) : 0.0;
+            }
+#pragma unroll
+            for (int u = 0; u < kCsrChunk / 32; ++u) {
+                const int k = lane + 32 * u;
+                if (k < cnt) s_prod[warp][k] = __dmul_rn(v[u], __ldg(x + cidx[u]));
             }
             __syncwarp();
             const i64 a0 = max(rs, cs), a1 = min(re, cs + cnt);
-            for (i64 k = a0; k < a1; ++k) s = acc_term(s, s_val[warp][k - cs], __ldg(x + s_col[warp][k - cs]));
+            for (i64 k = a0; k < a1; ++k) s = __dadd_rn(s, s_prod[warp][k - cs]);
             __syncwarp();
         }
         if (live) {
-            if (RESID) {
+            if (MODE == CSR_FIRST || MODE == CSR_MID) {
+                part_sum[row] = s;
+            } else if (RESID) {
                 const double r = __dsub_rn(b[row], s);
                 y[row] = r;
                 sq = fma(r, r, sq);
@@ -389,7 +411,7 @@ __global__ void __launch_bounds__(kBlock) csr_warp_kernel(i64 nloc, const int64_
             }
         }
     }
-    if (RESID) {
+    if (RESID && (MODE == CSR_ONLY || MODE == CSR_LAST)) {
         const double t = block_sum(sq);
         if (threadIdx.x == 0) partials[blockIdx.x] = t;
     }
@@ -567,12 +589,41 @@ int launch_csr(cudaStream_t s, i64 nloc, const int64_t* row_ptr, const int32_t* 
     const int grid = b ? reduce_grid()
                        : static_cast<int>(std::max<i64>(1, std::min<i64>(ceil_div(warps, kBlock / 32), i64(1) << 30)));
     if (b)
-        csr_warp_kernel<true><<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials);
+        csr_warp_kernel<CSR_ONLY, true, int64_t>
+            <<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials, nullptr);
     else
-        csr_warp_kernel<false><<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials);
+        csr_warp_kernel<CSR_ONLY, false, int64_t>
+            <<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials, nullptr);
     KB_LAUNCHED();
     ++launches;
     return b ? grid : 0;
+}
+
+int launch_csr_sliced(cudaStream_t s, i64 nloc, int nslices, const int32_t* const* row_ptr,
+                      const int32_t* const* col, const double* const* vals, const double* x, const double* b,
+                      double* y, double* partials, double* part_sum, int64_t& launches) {
+    const i64 warps = ceil_div(nloc, 32);
+    const int grid_free =
+        static_cast<int>(std::max<i64>(1, std::min<i64>(ceil_div(warps, kBlock / 32), i64(1) << 30)));
+    for (int p = 0; p < nslices; ++p) {
+        const bool first = p == 0, lastp = p == nslices - 1;
+        const int grid = (b && lastp) ? reduce_grid() : grid_free;
+        if (first)
+            csr_warp_kernel<CSR_FIRST, false, int32_t>
+                <<<grid, kBlock, 0, s>>>(nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
+        else if (!lastp)
+            csr_warp_kernel<CSR_MID, false, int32_t>
+                <<<grid, kBlock, 0, s>>>(nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
+        else if (b)
+            csr_warp_kernel<CSR_LAST, true, int32_t>
+                <<<grid, kBlock, 0, s>>>(nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
+        else
+            csr_warp_kernel<CSR_LAST, false, int32_t>
+                <<<grid, kBlock, 0, s>>>(nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
+        KB_LAUNCHED();
+        ++launches;
+    }
+    return b ? reduce_grid() : 0;
 }
 
 void launch_dot(cudaStream_t s, i64 n, const double* a, const double* b, double* partials,

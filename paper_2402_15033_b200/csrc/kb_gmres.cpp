@@ -191,9 +191,9 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
             } else {
                 const i64 c0 = (j == 0) ? 0 : store.filled() - 1;
                 cudaEvent_t t0 = ctx.begin_phase();
-                store.mpk(op, c0, s);
+                // fused MPK: one read of the start + s writes; else s SpMVs
+                rep.mpk_bytes += store.mpk(op, c0, s) ? 8.0 * op.nloc * (s + 1.0) : s * op.bytes_per_apply();
                 ctx.end_phase(PH_MPK, t0);
-                rep.mpk_bytes += s * op.bytes_per_apply();
                 cudaEvent_t t1 = ctx.begin_phase();
                 if (two_stage)
                     oc = store.preprocess_block(store.col(c0), store.ld(), s + 1, j != 0, rep.sync);

@@ -58,6 +58,13 @@ void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const 
 // CSR rows (row_ptr local, from 0) gathering x through int32 indices.
 int launch_csr(cudaStream_t s, i64 nloc, const int64_t* row_ptr, const int32_t* col, const double* vals,
                const double* x, const double* b, double* y, double* partials, int64_t& launches);
+// Column-sliced CSR (nslices ≥ 2): slice p holds each row's entries whose
+// (gathered) column lies in the p-th column range, in stored order, with its
+// own int32 row_ptr; the passes continue one running sum per row
+// (part_sum, nloc doubles) so every row is still summed in stored order.
+int launch_csr_sliced(cudaStream_t s, i64 nloc, int nslices, const int32_t* const* row_ptr,
+                      const int32_t* const* col, const double* const* vals, const double* x, const double* b,
+                      double* y, double* partials, double* part_sum, int64_t& launches);
 int reduce_grid();  // fixed grid of every partial-sum kernel (determinism)
 void launch_dot(cudaStream_t s, i64 n, const double* a, const double* b, double* partials,
                 int64_t& launches);

@@ -5,6 +5,8 @@
 // over NCCL send/recv (NVLink P2P) before the row kernel.
 #pragma once
 
+#include <vector>
+
 #include "kb_ctx.hpp"
 #include "kb_kernels.hpp"
 
@@ -20,6 +22,12 @@ struct Operator {
     // CSR
     DevBuf row_ptr, col, vals;
     DevBuf xfull, xsend;      // multi-rank gather of x
+    // Column-sliced copy of the CSR (nslices ≥ 2 when the gathered x is
+    // larger than the L2 share it should keep): one pass per column range,
+    // each pass's x slice stays L2-resident (k_ops.cu launch_csr_sliced).
+    int nslices = 1;
+    std::vector<DevBuf> s_row_ptr, s_col, s_vals;
+    DevBuf part_sum;          // running row sums between passes
     i64 max_rows = 0;
     DevBuf partials;          // Σr² partials of the residual mode
 

@@ -82,10 +82,11 @@ double* Store::scratch(int which, i64 w) {
     return scratch_[which].p;
 }
 
-void Store::mpk(Operator& op, i64 c0, i64 s) {
+bool Store::mpk(Operator& op, i64 c0, i64 s) {
     dim_check(c0 + s + 1 <= max_cols_, "basis store capacity exceeded");
-    if (op.mpk(col(c0), col(c0 + 1), ld_, static_cast<int>(s))) return;
+    if (op.mpk(col(c0), col(c0 + 1), ld_, static_cast<int>(s))) return true;
     for (i64 k = 0; k < s; ++k) op.apply(col(c0 + k), col(c0 + k + 1));
+    return false;
 }
 
 Outcome Store::append_block(const double* V, i64 ldv, i64 w, bool overlap, int kind, i64, Sync& sync) {

@@ -69,7 +69,8 @@ public:
     // z = R_jj⁻¹·y_panel.  Returns false when nothing is pending.
     bool deferred_coefficients(const std::vector<double>& y, std::vector<double>& y_out) const;
     // MPK into the store: column c0 holds the start; columns c0+1..c0+s.
-    void mpk(Operator& op, i64 c0, i64 s);
+    // Returns true when the fused one-pass kernel ran.
+    bool mpk(Operator& op, i64 c0, i64 s);
 
     // Telemetry: algorithmic BlkOrtho bytes for this rank.
     double ortho_bytes = 0.0;

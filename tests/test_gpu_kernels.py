@@ -58,6 +58,29 @@ def test_csr_spmv_bitwise(kb, ctx, ref, rng, n, per_row):
     np.testing.assert_array_equal(op.spmv(x), ref.spmv(a, x))
 
 
+# Column-sliced CSR (one pass per column range, running row sums carried
+# between passes; kb_operator.cpp): still bit-identical, including rows with
+# no entries in some slices, an empty row, the residual mode and the MPK.
+@pytest.mark.parametrize("n,per_row,slices", [(20000, 30, 2), (20000, 30, 3), (5000, 4, 7), (300, 0, 5),
+                                              (1, 0, 2)])
+def test_csr_sliced_bitwise(kb, ctx, ref, rng, monkeypatch, n, per_row, slices):
+    rp, ci, vv = random_csr(rng, n, per_row)
+    if n > 2:  # empty the middle row
+        i = n // 2
+        lo, hi = rp[i], rp[i + 1]
+        ci = np.concatenate([ci[:lo], ci[hi:]])
+        vv = np.concatenate([vv[:lo], vv[hi:]])
+        rp = rp.copy()
+        rp[i + 1:] -= hi - lo
+    a = ref.Csr(n, rp, ci, vv)
+    monkeypatch.setenv("KRY_CSR_SLICES", str(slices))
+    op = kb.CsrOperator(rp, ci, vv)
+    x = rng.standard_normal(n)
+    np.testing.assert_array_equal(op.spmv(x), ref.spmv(a, x))
+    start = x / np.linalg.norm(x)
+    np.testing.assert_array_equal(op.mpk(start, 3), ref.mpk(a, start, 3))
+
+
 def test_csr_laplace_matches_stencil(kb, ctx, ref, rng):
     a = ref.laplace2d(33, 21)
     csr = kb.CsrOperator(a.row_ptr, a.col_idx, a.vals)

@@ -97,6 +97,26 @@ def test_live_reference_small(kb, ctx, ref):
     assert abs(got.cycle_residuals[0] - want.cycle_residuals[0]) <= 1e-10 * want.cycle_residuals[0] + ABS_FLOOR
 
 
+def test_random_sparse_sliced_csr_identical(kb, ctx, monkeypatch):
+    """The column-sliced CSR passes (forced to 3 slices) reproduce the
+    unsliced solve bit for bit: same residual history to the last bit."""
+    import sys
+    sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+    from bench import random_sparse_rows
+    n = 20000
+    rp, ci, vv = random_sparse_rows(n, 0, n, 30)
+    reps = []
+    for slices in ("1", "3"):
+        monkeypatch.setenv("KRY_CSR_SLICES", slices)
+        op = kb.CsrOperator(rp, ci, vv)
+        b = op.spmv(np.ones(n))
+        reps.append(kb.sstep_gmres(op, b, None, kb.SolverConfig(scheme=kb.OrthoScheme(kb.OrthoKind(3), 60),
+                                                                  big_step=60, max_iters=600)))
+        del op
+    assert reps[0].cycle_residuals == reps[1].cycle_residuals
+    assert reps[0].iterations == reps[1].iterations
+
+
 def test_solution_quality(kb, ctx, ref):
     a = ref.laplace2d(64, 64)
     op = kb.Laplace2D(64, 64)

@@ -15,6 +15,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <mutex>
 #include <type_traits>
 
@@ -56,6 +57,9 @@ __device__ __forceinline__ double block_sum(double v) {
 __device__ __forceinline__ double acc_term(double s, double coeff, double x) {
     return __dadd_rn(s, __dmul_rn(coeff, x));
 }
+// acc_term(s, −1, x): −1·x is exact (a sign flip), so one add of −x gives
+// the same bits.
+__device__ __forceinline__ double sub_term(double s, double x) { return __dadd_rn(s, -x); }
 
 constexpr int kLinesPerThread = 8;
 
@@ -186,16 +190,16 @@ __global__ void __launch_bounds__(kBlock) stencil2d_vec_kernel(const StencilGeom
                 if (lane == 0 && ix > 0) left = x[i - 1];
                 if (lane == 31 && ix + 2 < nx) right = x[i + 2];
                 double s0 = 0.0, s1 = 0.0;
-                if (gl > 0) s0 = acc_term(s0, -1.0, down.x);
-                if (ix > 0) s0 = acc_term(s0, -1.0, left);
+                if (gl > 0) s0 = sub_term(s0, down.x);
+                if (ix > 0) s0 = sub_term(s0, left);
                 s0 = acc_term(s0, 4.0, cur.x);
-                s0 = acc_term(s0, -1.0, cur.y);
-                if (has_up) s0 = acc_term(s0, -1.0, up.x);
-                if (gl > 0) s1 = acc_term(s1, -1.0, down.y);
-                s1 = acc_term(s1, -1.0, cur.x);
+                s0 = sub_term(s0, cur.y);
+                if (has_up) s0 = sub_term(s0, up.x);
+                if (gl > 0) s1 = sub_term(s1, down.y);
+                s1 = sub_term(s1, cur.x);
                 s1 = acc_term(s1, 4.0, cur.y);
-                if (ix + 2 < nx) s1 = acc_term(s1, -1.0, right);
-                if (has_up) s1 = acc_term(s1, -1.0, up.y);
+                if (ix + 2 < nx) s1 = sub_term(s1, right);
+                if (has_up) s1 = sub_term(s1, up.y);
                 if (RESID) {
                     const double2 bb = *reinterpret_cast<const double2*>(b + i);
                     const double r0 = __dsub_rn(bb.x, s0), r1 = __dsub_rn(bb.y, s1);
@@ -209,6 +213,93 @@ __global__ void __launch_bounds__(kBlock) stencil2d_vec_kernel(const StencilGeom
             down = cur;
             cur = up;
             ++gl;
+        }
+    }
+    if (RESID) {
+        const double t = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+// 3-D 7-point stencil, two adjacent columns per thread (nx even): threads
+// tile one plane (pairs of one grid row, rows of the plane), each walks
+// kPlanesPerThread planes along z carrying the planes below and current in
+// registers (one new 16-byte load per plane from HBM); the y-neighbour rows
+// are the same plane's rows that neighbouring threads load (L1/L2 hits), the
+// x-neighbours come by shuffle.  Same per-row summation order as
+// stencil_kernel<3> (bit-identical).
+constexpr int kPlanesPerThread = 8;
+
+template <bool RESID>
+__global__ void __launch_bounds__(kBlock, 6) stencil3d_vec_kernel(const StencilGeom g, const double* __restrict__ x,
+                                                                  const double* __restrict__ halo_lo,
+                                                                  const double* __restrict__ halo_hi,
+                                                                  const double* __restrict__ b,
+                                                                  double* __restrict__ y,
+                                                                  double* __restrict__ partials) {
+    const int nx = static_cast<int>(g.nx), ny = static_cast<int>(g.ny), half = nx / 2;
+    const i64 plane = g.nx * g.ny;
+    const int q = blockIdx.x * kBlock + threadIdx.x;  // pair index inside a plane
+    const bool active = q < half * ny;
+    const int iy = active ? q / half : 0;
+    const int ix = active ? 2 * (q - iy * half) : 0;
+    const int off = iy * nx + ix;
+    const bool has_ym = iy > 0, has_yp = iy + 1 < ny, has_l = ix > 0, has_r = ix + 2 < nx;
+    const int lane = threadIdx.x & 31;
+    auto ld2 = [](const double* p) { return *reinterpret_cast<const double2*>(p); };
+    double sq = 0.0;
+    const int nzl = static_cast<int>(g.nzl), nz = static_cast<int>(g.nz), z0 = static_cast<int>(g.z0);
+    for (int zc = blockIdx.y * kPlanesPerThread; zc < nzl; zc += gridDim.y * kPlanesPerThread) {
+        const int zend = min(zc + kPlanesPerThread, nzl);
+        int gz = z0 + zc;
+        const double* xc = x + zc * plane + off;  // this thread's pair in the current plane
+        double* yc = y + zc * plane + off;
+        const double* bc = RESID ? b + zc * plane + off : nullptr;
+        double2 down = make_double2(0.0, 0.0), cur = make_double2(0.0, 0.0);
+        if (active) {
+            if (gz > 0) down = zc > 0 ? ld2(xc - plane) : ld2(halo_lo + off);
+            cur = ld2(xc);
+        }
+#pragma unroll 1
+        for (int l = zc; l < zend; ++l, ++gz, xc += plane, yc += plane) {
+            const bool has_dn = gz > 0, has_up = gz + 1 < nz;
+            double2 up = make_double2(0.0, 0.0);
+            if (active && has_up) up = l + 1 < nzl ? ld2(xc + plane) : ld2(halo_hi + off);
+            double left = __shfl_up_sync(0xffffffffu, cur.y, 1);
+            double right = __shfl_down_sync(0xffffffffu, cur.x, 1);
+            if (active) {
+                if (lane == 0 && has_l) left = xc[-1];
+                if (lane == 31 && has_r) right = xc[2];
+                const double2 ym = has_ym ? ld2(xc - nx) : make_double2(0.0, 0.0);
+                const double2 yp = has_yp ? ld2(xc + nx) : make_double2(0.0, 0.0);
+                double s0 = 0.0, s1 = 0.0;
+                if (has_dn) s0 = sub_term(s0, down.x);
+                if (has_ym) s0 = sub_term(s0, ym.x);
+                if (has_l) s0 = sub_term(s0, left);
+                s0 = acc_term(s0, 6.0, cur.x);
+                s0 = sub_term(s0, cur.y);
+                if (has_yp) s0 = sub_term(s0, yp.x);
+                if (has_up) s0 = sub_term(s0, up.x);
+                if (has_dn) s1 = sub_term(s1, down.y);
+                if (has_ym) s1 = sub_term(s1, ym.y);
+                s1 = sub_term(s1, cur.x);
+                s1 = acc_term(s1, 6.0, cur.y);
+                if (has_r) s1 = sub_term(s1, right);
+                if (has_yp) s1 = sub_term(s1, yp.y);
+                if (has_up) s1 = sub_term(s1, up.y);
+                if (RESID) {
+                    const double2 bb = ld2(bc);
+                    bc += plane;
+                    const double r0 = __dsub_rn(bb.x, s0), r1 = __dsub_rn(bb.y, s1);
+                    *reinterpret_cast<double2*>(yc) = make_double2(r0, r1);
+                    sq = fma(r0, r0, sq);
+                    sq = fma(r1, r1, sq);
+                } else {
+                    *reinterpret_cast<double2*>(yc) = make_double2(s0, s1);
+                }
+            }
+            down = cur;
+            cur = up;
         }
     }
     if (RESID) {
@@ -507,9 +598,15 @@ StencilGeom make_stencil_geom(int dims, i64 nx, i64 ny, i64 nz, i64 row_begin, i
     return g;
 }
 
+dim3 stencil3d_vec_grid(const StencilGeom& g) {
+    const i64 chunks = std::max<i64>(1, ceil_div(g.nzl, kPlanesPerThread));
+    return dim3(static_cast<unsigned>(ceil_div(g.nx / 2 * g.ny, kBlock)),
+                static_cast<unsigned>(std::min<i64>(chunks, 65535)));
+}
+
 int stencil_partials(const StencilGeom& g) {
-    const dim3 d = stencil_grid(g);
-    return static_cast<int>(d.x * d.y);
+    const dim3 d = stencil_grid(g), v = stencil3d_vec_grid(g);
+    return static_cast<int>(std::max(d.x * d.y, g.dims == 3 ? v.x * v.y : 0u));
 }
 
 int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const double* halo_lo,
@@ -522,6 +619,20 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
             stencil2d_vec_kernel<true><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
         else
             stencil2d_vec_kernel<false><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+        KB_LAUNCHED();
+        ++launches;
+        return b ? static_cast<int>(grid.x * grid.y) : 0;
+    }
+    static const bool vec3 = [] {
+        const char* e = std::getenv("KRY_STENCIL3D_VEC");
+        return !e || std::atoi(e) != 0;
+    }();
+    if (vec3 && g.dims == 3 && (g.nx & 1) == 0 && g.nx * g.ny < (i64(1) << 30) && g.nzl < (i64(1) << 30) && a16(x) && a16(y) && a16(b) && a16(halo_lo) && a16(halo_hi)) {
+        const dim3 grid = stencil3d_vec_grid(g);
+        if (b)
+            stencil3d_vec_kernel<true><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+        else
+            stencil3d_vec_kernel<false><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
         KB_LAUNCHED();
         ++launches;
         return b ? static_cast<int>(grid.x * grid.y) : 0;

@@ -27,7 +27,9 @@ def test_laplace2d_stencil_bitwise(kb, ctx, ref, rng, nx, ny):
     np.testing.assert_array_equal(op.spmv(x), ref.spmv(a, x))
 
 
-@pytest.mark.parametrize("dims", [(2, 2, 2), (5, 3, 4), (17, 9, 11), (64, 64, 64)])
+@pytest.mark.parametrize("dims", [(2, 2, 2), (5, 3, 4), (17, 9, 11), (64, 64, 64),
+                                  # vectorised kernel: warps straddling grid rows, long z walks
+                                  (6, 5, 7), (10, 33, 4), (130, 3, 19), (4, 2, 40)])
 def test_laplace3d_stencil_bitwise(kb, ctx, ref, rng, dims):
     a = ref.laplace3d(*dims)
     op = kb.Laplace3D(*dims)

@@ -1,3 +1,5 @@
+#include <cstdlib>
+#include <chrono>
 #include "kb_ctx.hpp"
 
 #include <cstring>
@@ -14,6 +16,7 @@ namespace kb {
     } while (0)
 
 Ctx::Ctx(int dev, int nr, int rk, const void* nccl_id) : device(dev), nranks(nr), rank(rk) {
+    if (const char* e = std::getenv("KRY_HOST_PROFILE")) host_profile = std::atoi(e) != 0;
     int count = 0;
     if (cudaGetDeviceCount(&count) != cudaSuccess || count == 0) {
         cudaGetLastError();
@@ -50,7 +53,17 @@ Ctx::~Ctx() {
 
 void bind_device(Ctx& c) { KB_CUDA(cudaSetDevice(c.device)); }
 
-void Ctx::sync() { KB_CUDA(cudaStreamSynchronize(stream)); }
+void Ctx::sync() {
+    drain_timers();  // elapsed-time queries of finished phases, while the GPU is still busy
+    if (!host_profile) {
+        KB_CUDA(cudaStreamSynchronize(stream));
+        return;
+    }
+    const auto t0 = std::chrono::steady_clock::now();
+    KB_CUDA(cudaStreamSynchronize(stream));
+    sync_wait_s += std::chrono::duration<double>(std::chrono::steady_clock::now() - t0).count();
+    ++sync_count;
+}
 
 cudaEvent_t Ctx::begin_phase() {
     if (!timing) return nullptr;
@@ -76,6 +89,21 @@ void Ctx::end_phase(int phase, cudaEvent_t start) {
     }
     KB_CUDA(cudaEventRecord(e, stream));
     pending.push_back({phase, start, e});
+}
+
+void Ctx::drain_timers() {
+    size_t done = 0;
+    for (; done < pending.size(); ++done) {  // events complete in stream order
+        const Pending& p = pending[done];
+        if (cudaEventQuery(p.b) != cudaSuccess) break;
+        float ms = 0.f;
+        KB_CUDA(cudaEventElapsedTime(&ms, p.a, p.b));
+        seconds[p.phase] += ms * 1e-3;
+        pool.push_back(p.a);
+        pool.push_back(p.b);
+    }
+    cudaGetLastError();  // cudaErrorNotReady from the query is not an error
+    pending.erase(pending.begin(), pending.begin() + static_cast<std::ptrdiff_t>(done));
 }
 
 void Ctx::resolve_timers() {

@@ -94,10 +94,15 @@ struct Ctx {
     ~Ctx();
 
     void sync();
+    // KRY_HOST_PROFILE=1: time spent blocked in sync() (printed by gmres()).
+    bool host_profile = false;
+    double sync_wait_s = 0.0;
+    int64_t sync_count = 0;
     // Timer: begin() returns a token; end(token) closes it.
     cudaEvent_t begin_phase();
     void end_phase(int phase, cudaEvent_t start);
     void resolve_timers();  // after a stream sync: accumulate elapsed times
+    void drain_timers();    // accumulate the phases that already finished (no wait)
 
     // Σ over ranks, in place on the device (no-op for one rank).
     void allreduce_sum(double* d, size_t count);

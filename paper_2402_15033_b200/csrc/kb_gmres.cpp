@@ -1,5 +1,7 @@
 #include "kb_gmres.hpp"
 
+#include <cstdio>
+
 #include <chrono>
 #include <cmath>
 #include <limits>
@@ -39,6 +41,9 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
     }
     validate_config(cfg);
     const auto t_start = std::chrono::steady_clock::now();
+    const auto prof_t0 = t_start;
+    const int64_t prof_syncs0 = ctx.sync_count, prof_launch0 = ctx.launches;
+    const double prof_wait0 = ctx.sync_wait_s;
     const i64 n = op.nloc;
     const i64 m = cfg.restart_len;
     const i64 s = standard_mode ? 1 : cfg.step;
@@ -113,16 +118,30 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
     };
 
     // gmres.hpp:247-269
+    // The unforced check after a cycle's last block and the forced one that
+    // follows it see the same store: the host H / LSQ of the first is reused.
+    struct LsqCache {
+        i64 reduces = -1, filled = -1;
+        double gamma = 0.0;
+        Lsq lsq;
+        std::vector<double> ycoef;
+    } cache;
     auto check_and_update = [&](double gamma, bool force) -> Check {
         Check res;
         const i64 k = usable_cols();
         if (k == 0) return res;
-        Mat h = assemble_hessenberg(store.coefficients(), k, store.block_records());
-        Lsq lsq = solve_hessenberg_lsq(h, gamma);
-        // A deferred last-panel finalize: the same x update over the stored
-        // (preprocessed) columns with transformed coefficients.
-        std::vector<double> ycoef;
-        if (!store.deferred_coefficients(lsq.y, ycoef)) ycoef = lsq.y;
+        if (!(cache.reduces == rep.sync.reduces && cache.filled == store.filled() && cache.gamma == gamma)) {
+            Mat h = assemble_hessenberg(store.coefficients(), k, store.block_records());
+            cache.lsq = solve_hessenberg_lsq(h, gamma);
+            // A deferred last-panel finalize: the same x update over the stored
+            // (preprocessed) columns with transformed coefficients.
+            if (!store.deferred_coefficients(cache.lsq.y, cache.ycoef)) cache.ycoef = cache.lsq.y;
+            cache.reduces = rep.sync.reduces;
+            cache.filled = store.filled();
+            cache.gamma = gamma;
+        }
+        const Lsq& lsq = cache.lsq;
+        const std::vector<double>& ycoef = cache.ycoef;
         res.implicit_crossed = lsq.implicit_residual <= cfg.rel_tol * r0;
         if (!res.implicit_crossed && !force) return res;
 
@@ -257,7 +276,6 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         if (!updated_this_cycle) check_and_update(gamma, true);
         const double rnorm = r_norm;
         rep.cycle_residuals.push_back(rnorm / r0);
-        ctx.resolve_timers();
         if (done) break;
         ++rep.restarts;
         if (rnorm / r0 <= cfg.rel_tol) {
@@ -279,6 +297,13 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         rep.reduces_per_iteration = static_cast<double>(rep.sync.reduces) / static_cast<double>(rep.iterations);
     rep.ortho_bytes = store.ortho_bytes;
     finish();
+    if (ctx.host_profile) {
+        const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - prof_t0).count();
+        std::fprintf(stderr,
+                     "[kry host profile] wall %.6f s, blocked in %lld syncs %.6f s, launches %lld, cycles %lld\n",
+                     wall, static_cast<long long>(ctx.sync_count - prof_syncs0), ctx.sync_wait_s - prof_wait0,
+                     static_cast<long long>(ctx.launches - prof_launch0), static_cast<long long>(rep.restarts + 1));
+    }
     return rep;
 }
 

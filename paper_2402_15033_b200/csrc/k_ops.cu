@@ -17,6 +17,7 @@
 #include <algorithm>
 #include <cstdlib>
 #include <mutex>
+#include <unordered_map>
 #include <type_traits>
 
 #include "kb_common.hpp"
@@ -654,10 +655,41 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
     return b ? static_cast<int>(grid.x * grid.y) : 0;
 }
 
-bool mpk2d_supported(const StencilGeom& g, int s, const double* x, const double* out, i64 ldo) {
+int occupancy(const void* kernel, int threads, size_t smem) {
+    struct Key {
+        const void* k;
+        int t;
+        size_t s;
+        bool operator==(const Key& o) const { return k == o.k && t == o.t && s == o.s; }
+    };
+    struct Hash {
+        size_t operator()(const Key& k) const {
+            return std::hash<const void*>()(k.k) * 31u ^ std::hash<size_t>()(k.s * 4099u + static_cast<size_t>(k.t));
+        }
+    };
+    static std::mutex mu;
+    static std::unordered_map<Key, int, Hash> cache;
+    std::lock_guard<std::mutex> lock(mu);
+    const Key key{kernel, threads, smem};
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    int per_sm = 0;
+    KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, threads, smem));
+    cache.emplace(key, per_sm);
+    return per_sm;
+}
+
+bool mpk2d_supported(const StencilGeom& g, int s, const double* x, const double* out, i64 ldo, bool force) {
     auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    return g.dims == 2 && (g.nx & 1) == 0 && s >= 1 && s <= 8 && (ldo & 1) == 0 && a16(x) && a16(out) &&
-           g.lines >= 1 && g.nx + 64 < (i64(1) << 31) && g.ny + 64 < (i64(1) << 31);
+    if (!(g.dims == 2 && (g.nx & 1) == 0 && s >= 1 && s <= 8 && (ldo & 1) == 0 && a16(x) && a16(out) &&
+          g.lines >= 1 && g.nx + 64 < (i64(1) << 31) && g.ny + 64 < (i64(1) << 31)))
+        return false;
+    // Worth it only with at least one wave of (window, band) tasks: each
+    // warp's wavefront is a serial chain, so small grids (512²: 250 tasks,
+    // 24 µs per block vs 19 µs for five SpMVs) stay on the per-SpMV kernels.
+    const int h = (s + 1) & ~1;
+    const i64 tasks = ceil_div(g.nx, 64 - 2 * h) * std::max<i64>(1, g.lines / (4 * s));
+    return force || tasks >= static_cast<i64>(num_sms()) * 16;
 }
 
 void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const double* halo_lo,
@@ -668,8 +700,7 @@ void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const 
         // One wave of resident warps, one (window, band) task each: bands as
         // tall as that allows (the 2s-line band overlap is recomputed), at
         // least 4s lines; very wide grids loop over tasks.
-        int per_sm = 0;
-        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, kBlock, 0));
+        const int per_sm = occupancy(reinterpret_cast<const void*>(kernel), kBlock, 0);
         const i64 resident = static_cast<i64>(num_sms()) * std::max(per_sm, 1) * (kBlock / 32);
         const i64 nbands = std::max<i64>(1, std::min<i64>(resident / nwx, g.lines / (4 * s)));
         const i64 band = ceil_div(g.lines, nbands);

@@ -649,7 +649,40 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
+CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows);
+
+// Tensor maps are cached by their parameters: the solver re-launches the same
+// (store column, shape) combinations every cycle, and an encode costs more
+// host time than the launch itself.
 CUtensorMap make_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows) {
+    struct Key {
+        const double* base;
+        i64 ld, rows, cols;
+        int box;
+        bool operator==(const Key& o) const {
+            return base == o.base && ld == o.ld && rows == o.rows && cols == o.cols && box == o.box;
+        }
+    };
+    struct Hash {
+        size_t operator()(const Key& k) const {
+            size_t h = std::hash<const void*>()(k.base);
+            for (i64 v : {k.ld, k.rows, k.cols, static_cast<i64>(k.box)}) h = h * 1000003u ^ std::hash<i64>()(v);
+            return h;
+        }
+    };
+    static std::mutex mu;
+    static std::unordered_map<Key, CUtensorMap, Hash> cache;
+    const Key key{base, ld, rows, cols, box_rows};
+    std::lock_guard<std::mutex> lock(mu);
+    auto it = cache.find(key);
+    if (it != cache.end()) return it->second;
+    if (cache.size() > 4096) cache.clear();
+    CUtensorMap m = encode_map(base, ld, rows, cols, box_rows);
+    cache.emplace(key, m);
+    return m;
+}
+
+CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
     if (cols <= 0 || base == nullptr) return m;  // unused operand
@@ -830,8 +863,7 @@ void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp,
     const i64 rows_per_thread = vec ? 2 : 1;
     auto go = [&](auto kernel) {
         set_smem(reinterpret_cast<const void*>(kernel), smem);
-        int per_sm = 0;
-        KB_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kernel, 256, smem));
+        const int per_sm = occupancy(reinterpret_cast<const void*>(kernel), 256, smem);
         const i64 want = ceil_div(n, (wmax == 64 ? 128 : 256) * rows_per_thread);
         const int grid = static_cast<int>(std::max<i64>(1, std::min<i64>(want, static_cast<i64>(sm_count()) * std::max(per_sm, 1))));
         kernel<<<grid, 256, smem, stream>>>(n, P, ldp, static_cast<int>(cp), V, ldv, static_cast<int>(w), d_coef,

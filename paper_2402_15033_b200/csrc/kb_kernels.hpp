@@ -11,6 +11,10 @@
 
 namespace kb {
 
+// Resident blocks per SM of a kernel at a block size / dynamic smem (cached:
+// the occupancy query costs microseconds of host time per launch).
+int occupancy(const void* kernel, int threads, size_t smem);
+
 // ---- k_tsqr.cu : BlkOrtho (K3 Gram, K5 update) ---------------------------
 std::vector<std::pair<i64, i64>> prefix_groups(i64 c0, i64 w);
 i64 gram_scratch_doubles(i64 w);
@@ -52,7 +56,8 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
 int stencil_partials(const StencilGeom& g);
 // Fused 2-D MPK: out[:, k−1] = A^k·x, k = 1..s (out columns ldo apart), one
 // pass; halos hold s lines each (multi-rank).
-bool mpk2d_supported(const StencilGeom& g, int s, const double* x, const double* out, i64 ldo);
+// force: skip the size heuristic (tests).
+bool mpk2d_supported(const StencilGeom& g, int s, const double* x, const double* out, i64 ldo, bool force);
 void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const double* halo_lo,
                   const double* halo_hi, double* out, i64 ldo, int s, int64_t& launches);
 // CSR rows (row_ptr local, from 0) gathering x through int32 indices.

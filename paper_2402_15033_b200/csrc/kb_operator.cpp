@@ -230,14 +230,15 @@ int Operator::apply(const double* x, double* y, const double* b) {
 }
 
 bool Operator::mpk(const double* x, double* out, i64 ldo, int s) {
-    static const bool enabled = [] {
-        const char* e = std::getenv("KRY_FUSED_MPK");
-        return !e || std::atoi(e) != 0;
-    }();
+    // KRY_FUSED_MPK: 0 = never, 1 (default) = when the grid is large enough
+    // to fill the GPU with wavefront tasks, 2 = whenever supported (tests).
+    const char* e = std::getenv("KRY_FUSED_MPK");
+    const int mode = e ? std::atoi(e) : 1;
     Ctx& c = *ctx;
     // Every rank must own at least s lines (the halo is the neighbour's s
     // edge lines); the partition differs by at most one line between ranks.
-    if (!enabled || kind != LAPLACE2D || geom.ny / c.nranks < s || !mpk2d_supported(geom, s, x, out, ldo))
+    if (mode == 0 || kind != LAPLACE2D || geom.ny / c.nranks < s ||
+        !mpk2d_supported(geom, s, x, out, ldo, mode == 2))
         return false;
     const i64 h = static_cast<i64>(s) * geom.nx;
     if (c.nranks > 1) {

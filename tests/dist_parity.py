@@ -20,6 +20,10 @@ sys.path.insert(0, os.path.dirname(os.path.abspath(__file__)))
 
 import paper_2402_15033_b200 as kb  # noqa: E402
 
+# The grids here are below the fused-MPK size heuristic: force the fused
+# 2-D kernel (s-line halos) so the row-partitioned solves exercise it.
+os.environ["KRY_FUSED_MPK"] = "2"
+
 GOLDEN = json.load(open(os.path.join(ROOT, "tests", "golden", "solver_golden.json")))
 CONFIGS = ["two_2d100_s60", "two_2d100_s20", "pip2_2d64", "two_3d16_s60", "two_2d48_csr", "standard_2d32",
            "two_2d128_s60"]

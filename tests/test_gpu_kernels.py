@@ -107,7 +107,8 @@ def test_mpk_bitwise(kb, ctx, ref, rng, s):
                                      (106, 41, 1), (64, 9, 6), (2, 2, 3),
                                      # a window's last lane on the grid's last column
                                      (110, 40, 5), (58, 30, 6), (104, 50, 8), (60, 33, 3), (62, 20, 1)])
-def test_mpk_fused_bitwise(kb, ctx, ref, rng, nx, ny, s):
+def test_mpk_fused_bitwise(kb, ctx, ref, rng, monkeypatch, nx, ny, s):
+    monkeypatch.setenv("KRY_FUSED_MPK", "2")  # below the size heuristic: force the fused kernel
     a = ref.laplace2d(nx, ny)
     op = kb.Laplace2D(nx, ny)
     start = rng.standard_normal(a.n)

@@ -70,6 +70,16 @@ def test_solver_matches_reference(kb, ctx, ref, key):
     assert_parity(rep, g)
 
 
+# The golden grids are below the fused-MPK size heuristic; run the 2-D
+# stencil configurations again with the fused one-pass MPK forced on.
+@pytest.mark.parametrize("key", sorted(k for k in GOLDEN if GOLDEN[k]["operator"] != "csr"
+                                       and GOLDEN[k]["dims"] == 2 and not GOLDEN[k]["standard"]))
+def test_solver_matches_reference_fused_mpk(kb, ctx, ref, monkeypatch, key):
+    monkeypatch.setenv("KRY_FUSED_MPK", "2")
+    rep, g = run_golden(kb, ref, key)
+    assert_parity(rep, g)
+
+
 def test_survey_anchors(kb, ctx, ref):
     # SURVEY §8(c) measured anchors at 100²
     assert (GOLDEN["pip2_2d100"]["iterations"], GOLDEN["pip2_2d100"]["restarts"],

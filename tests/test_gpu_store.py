@@ -176,3 +176,33 @@ def test_store_config_errors(kb, ctx):
     st = kb.BasisStore(10, 6, 3, 6)
     with pytest.raises(kb.DimensionMismatch):
         st.append_block(np.ones((10, 8)), False, kb.OrthoScheme(), kb.SyncCounter())  # capacity
+
+
+@pytest.mark.parametrize("grid,kind,shat", [(64, 2, 0), (64, 3, 60), (100, 3, 20), (128, 3, 60), (128, 2, 0)])
+def test_orthogonality_error_protocol(kb, ctx, ref, grid, kind, shat):
+    """on the same MPK-fed blocks (one full m = 60 cycle),
+    ‖I − QᵀQ‖₂ of the device store is ≤ max(1e-12, 10× the reference
+    store's) and within 1e-10 absolute of it (ortho_error, spectral.hpp:104)."""
+    m, s = 60, 5
+    a = ref.laplace2d(grid, grid)
+    n = a.n
+    b = ref.spmv(a, np.ones(n))
+    v1 = b / np.linalg.norm(b)
+    eff = shat if shat else m
+    st = kb.BasisStore(n, m, s, eff)
+    rs = ref.Store(n, m, s, eff)
+    sync = kb.SyncCounter()
+    for j in range(m // s):
+        blk = ref.mpk(a, v1 if j == 0 else rs.column(rs.info().filled - 1), s)
+        if kind == 3:
+            assert not st.preprocess_block(blk, j != 0, sync).breakdown
+            rs.preprocess_block(blk, j != 0)
+            if rs.info().big_panel_full or j + 1 == m // s:
+                st.finalize_big_panel(sync)
+                rs.finalize_big_panel()
+        else:
+            assert not st.append_block(blk, j != 0, kb.OrthoScheme(kb.OrthoKind(kind), 0), sync).breakdown
+            rs.append_block(blk, j != 0, kind)
+    e_gpu, e_cpu = ref.ortho_error(st.all()), ref.ortho_error(rs.all())
+    assert e_gpu <= max(1e-12, 10.0 * e_cpu), (e_gpu, e_cpu)
+    assert abs(e_gpu - e_cpu) <= 1e-10

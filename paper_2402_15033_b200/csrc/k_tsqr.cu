@@ -462,7 +462,8 @@ __device__ __forceinline__ void update_rows(i64 row, const double* __restrict__ 
 template <int WMAX, int R>
 __global__ void __launch_bounds__(256)
     update_kernel(i64 n, const double* __restrict__ P, i64 ldp, int cp, const double* V, i64 ldv, int w,
-                  const double* __restrict__ coef, int triangular, double* out, i64 ldo) {
+                  const double* __restrict__ coef, int triangular, double* out, i64 ldo, const int* skip) {
+    if (skip && *skip) return;  // speculative block whose factorisation failed (k_pip.cu)
     // Columns w ≤ j < WMAX are identity padding (zero coefficients, inv = 1):
     // the arithmetic below is branch-free and leaves them at zero.
     extern __shared__ __align__(16) double c_sm[];
@@ -492,7 +493,8 @@ __global__ void __launch_bounds__(256)
 // inv[2][32].
 __global__ void __launch_bounds__(256)
     update_pair_kernel(i64 n, const double* __restrict__ P, i64 ldp, int cp, const double* V, i64 ldv, int w,
-                       const double* __restrict__ coef, int triangular, double* out, i64 ldo) {
+                       const double* __restrict__ coef, int triangular, double* out, i64 ldo, const int* skip) {
+    if (skip && *skip) return;
     constexpr int H = 32;
     extern __shared__ __align__(16) double c_sm[];
     const int ncoef = (cp + 64 + 1) * 64;
@@ -851,7 +853,8 @@ static int update_rows_setting() {  // KRY_UPDATE_ROWS=1 → one row per thread 
 int update_wmax(i64 w) { return w <= 6 ? 6 : w <= 8 ? 8 : w <= 16 ? 16 : w <= 32 ? 32 : 64; }
 
 void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
-                   i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches) {
+                   i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches,
+                   const int* skip) {
     const int wmax = update_wmax(w);
     const size_t smem = static_cast<size_t>(round_up(cp, 12) + wmax + 1) * wmax * 8;
     if (smem > 200 * 1024) fail(KRY_UNSUPPORTED, "update coefficients exceed shared memory");
@@ -867,7 +870,7 @@ void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp,
         const i64 want = ceil_div(n, (wmax == 64 ? 128 : 256) * rows_per_thread);
         const int grid = static_cast<int>(std::max<i64>(1, std::min<i64>(want, static_cast<i64>(sm_count()) * std::max(per_sm, 1))));
         kernel<<<grid, 256, smem, stream>>>(n, P, ldp, static_cast<int>(cp), V, ldv, static_cast<int>(w), d_coef,
-                                            triangular ? 1 : 0, out, ldo);
+                                            triangular ? 1 : 0, out, ldo, skip);
     };
     switch (wmax) {
         case 6: vec ? go(update_kernel<6, 2>) : go(update_kernel<6, 1>); break;

@@ -169,6 +169,10 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         return res;
     };
 
+    static const bool speculate_default = [] {  // KRY_SPECULATE=0: every block waits for its factorisation
+        const char* e = std::getenv("KRY_SPECULATE");
+        return !(e && std::string(e) == "0");
+    }();
     static const bool defer_last = [] {
         const char* e = std::getenv("KRY_DEFER_FINALIZE");
         return !(e && std::string(e) == "0");
@@ -196,9 +200,42 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         if (standard_mode) store.seed_unit_column(store.col(0));
 
         bool updated_this_cycle = false;
+        bool speculate = speculate_default && two_stage && store.can_speculate(s + 1);
+        bool skip_mpk = false;  // a speculative block being redone: its raw columns are in place
         for (i64 j = 0; j < blocks && !done; ++j) {
             Outcome oc;
-            if (standard_mode) {
+            if (speculate) {
+                // Queue the rest of the big panel without waiting: device
+                // factorisation + gated updates (Store::preprocess_speculative),
+                // then one sync replays the bookkeeping.  A failed block is
+                // redone on the synchronous path below, which handles the
+                // truncation / breakdown exactly as the reference.
+                const i64 j0 = j;
+                i64 jj = j;
+                for (;;) {
+                    const i64 c0 = (jj == 0) ? 0 : store.spec_filled() - 1;
+                    cudaEvent_t t0 = ctx.begin_phase();
+                    rep.mpk_bytes += store.mpk(op, c0, s) ? 8.0 * op.nloc * (s + 1.0) : s * op.bytes_per_apply();
+                    ctx.end_phase(PH_MPK, t0);
+                    cudaEvent_t t1 = ctx.begin_phase();
+                    store.preprocess_speculative(s + 1, jj != 0);
+                    ctx.end_phase(PH_ORTHO, t1);
+                    ++jj;
+                    if (store.spec_panel_full() || jj == blocks) break;
+                }
+                cudaEvent_t t1 = ctx.begin_phase();
+                const i64 f = store.resolve_speculative(rep.sync);
+                ctx.end_phase(PH_ORTHO, t1);
+                rep.iterations += s * (f < 0 ? jj - j0 : f);
+                if (f >= 0) {
+                    speculate = false;
+                    skip_mpk = true;
+                    j = j0 + f - 1;  // ++j: the failed block, synchronously
+                    continue;
+                }
+                j = jj - 1;  // the panel's last block: finalize / check below
+                oc.committed = s + 1;
+            } else if (standard_mode) {
                 const i64 f = store.filled();
                 cudaEvent_t t0 = ctx.begin_phase();
                 op.apply(store.col(f - 1), store.col(f));
@@ -209,10 +246,13 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
                 ctx.end_phase(PH_ORTHO, t1);
             } else {
                 const i64 c0 = (j == 0) ? 0 : store.filled() - 1;
-                cudaEvent_t t0 = ctx.begin_phase();
-                // fused MPK: one read of the start + s writes; else s SpMVs
-                rep.mpk_bytes += store.mpk(op, c0, s) ? 8.0 * op.nloc * (s + 1.0) : s * op.bytes_per_apply();
-                ctx.end_phase(PH_MPK, t0);
+                if (!skip_mpk) {
+                    cudaEvent_t t0 = ctx.begin_phase();
+                    // fused MPK: one read of the start + s writes; else s SpMVs
+                    rep.mpk_bytes += store.mpk(op, c0, s) ? 8.0 * op.nloc * (s + 1.0) : s * op.bytes_per_apply();
+                    ctx.end_phase(PH_MPK, t0);
+                }
+                skip_mpk = false;
                 cudaEvent_t t1 = ctx.begin_phase();
                 if (two_stage)
                     oc = store.preprocess_block(store.col(c0), store.ld(), s + 1, j != 0, rep.sync);
@@ -221,7 +261,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
                                             cfg.scheme_big_panel_size, rep.sync);
                 ctx.end_phase(PH_ORTHO, t1);
             }
-            rep.iterations += s;
+            if (!speculate) rep.iterations += s;  // (the speculative branch counted its blocks)
 
             if (oc.breakdown || oc.truncated) {
                 rep.breakdown = true;

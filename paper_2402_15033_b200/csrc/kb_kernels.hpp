@@ -32,8 +32,29 @@ int update_wmax(i64 w);
 void launch_update_mma(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
                        i64 w, const double* d_mfrag, double* out, i64 ldo, int64_t& launches);
 // out = (V − P·R_col)·R_jj⁻¹ (triangular) or V − P·R_col; out may alias V.
+// skip (device flag, optional): the kernel returns without writing when *skip != 0.
 void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
-                   i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches);
+                   i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches,
+                   const int* skip = nullptr);
+
+// ---- k_pip.cu : device BCGS-PIP factorisation (speculative first stage) --
+// Result slot of one block (doubles): [kSlotStatus] 0 = committed, p > 0 =
+// Cholesky pivot p failed, −1 = an earlier block of the chain failed;
+// [kSlotRcol …] R_col (c0×w) then R_jj (w×w), column-major; [kSlotPieces …]
+// the panel-Gram pieces P[:,0:c0]ᵀ·P[:, x_first:x_first+x_count] (c0×x_count).
+constexpr int kSlotStatus = 0, kSlotRcol = 8, kSlotPieces = 8 + 64 * 8 + 64, kSlotDoubles = 2048;
+struct PipBlockArgs {
+    const double* packed;     // reduced (and allreduced) packed Gram tiles of the block
+    int nb;                   // slot blocks: 1 (V) + prefix blocks; regular tiles = nb
+    int nx, xb0;              // extra prefix column blocks (panel-Gram pieces)
+    int x_first, x_count;
+    int c0, w, wmax;          // wmax: K5 column padding (update_wmax)
+    double* slot;
+    const double* prev_slot;  // the previous speculative block's slot, or nullptr
+    double* coef;             // K5 coefficients for this block's update
+    int* skip;                // K5 skip flag: set when this block (or an earlier one) failed
+};
+void launch_pip_block(cudaStream_t stream, const PipBlockArgs& a, int64_t& launches);
 
 // ---- k_ops.cu : operators (K1/K2), restart-loop vectors (K8-K10) ---------
 struct StencilGeom {

@@ -4,6 +4,7 @@
 #include <cstdlib>
 #include <cstring>
 
+#include "kb_kernels.hpp"
 #include "kb_ortho.hpp"
 
 namespace kb {
@@ -54,6 +55,7 @@ bool Store::deferred_coefficients(const std::vector<double>& y, std::vector<doub
 
 void Store::reset() {
     pending_ = false;
+    spec_.clear();
     std::fill(pready_.begin(), pready_.end(), 0);
     filled_ = 0;
     finalized_ = 0;
@@ -80,6 +82,123 @@ void Store::seed_unit_column(const double* d_v) {
 double* Store::scratch(int which, i64 w) {
     scratch_[which].ensure(static_cast<size_t>(ld_) * round_up(w, 8) * 8);
     return scratch_[which].p;
+}
+
+bool Store::can_speculate(i64 w) const {
+    // one prefix group (round_up(c0,8) + 8 ≤ 64) for every block of the
+    // cycle, and the fused panel-Gram bookkeeping this path assumes
+    return w >= 1 && w <= 8 && max_cols_ <= 64 && fused_panel_gram_;
+}
+
+bool Store::spec_panel_full() const {
+    const i64 f = spec_filled(), b = spec_.empty() ? big_panel_start_ : spec_bps_;
+    return f > b && f - b >= big_panel_size_ + 1;
+}
+
+void Store::preprocess_speculative(i64 w, bool overlap) {
+    const bool first = spec_.empty();
+    const i64 filled = first ? filled_ : spec_filled_;
+    if (overlap && filled == 0) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: basis store capacity exceeded");
+    const i64 c0 = overlap ? filled - 1 : filled;
+    if (c0 + w > max_cols_) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: basis store capacity exceeded");
+    const i64 maxb = max_cols_;  // queue capacity (blocks per cycle ≤ m)
+    if (first) {
+        spec_bps_ = big_panel_start_;
+        spec_xd_ = big_panel_start_;
+        while (spec_xd_ < max_cols_ && pready_[static_cast<size_t>(spec_xd_)]) ++spec_xd_;
+        spec_slots_.ensure(static_cast<size_t>(maxb) * kSlotDoubles * 8);
+        spec_coef_.ensure(static_cast<size_t>(maxb) * 640 * 8);
+        spec_skip_.ensure(static_cast<size_t>(maxb) * 4);
+        spec_host_.ensure(static_cast<size_t>(maxb) * kSlotDoubles * 8);
+    }
+    const i64 idx = static_cast<i64>(spec_.size());
+    // panel-Gram pieces (same rule as run_scheme's first-stage branch): the
+    // previous block is a preprocessed block of the open panel unless this
+    // is the panel's first block
+    const bool prev_in_panel = !first || (!records_.empty() && states_.back() == KRY_PANEL_PREPROCESSED);
+    i64 xf = -1, xc = 0;
+    if (prev_in_panel) {
+        const i64 xend = std::min(c0 / 8 * 8, spec_xd_ / 8 * 8 + 16);
+        if (xend > spec_xd_) {
+            xf = spec_xd_;
+            xc = xend - spec_xd_;
+        }
+    }
+    // Gram (+ reduce) → allreduce → device factorisation → gated update
+    std::vector<int> tiles;
+    ctx_.gram_partials.ensure(static_cast<size_t>(gram_scratch_doubles(w)) * 8);
+    ctx_.gram_packed.ensure(2 * 64 * 64 * 8);
+    cudaEvent_t t0 = ctx_.begin_phase();
+    launch_gram_pass(ctx_.stream, n_, c0 > 0 ? col(0) : nullptr, ld_, c0, col(c0), ld_, w, true,
+                     ctx_.gram_partials.p, ctx_.gram_packed.p, tiles, ctx_.launches, xf, xc);
+    ctx_.end_phase(PH_GRAM, t0);
+    ctx_.gram_bytes += 8.0 * n_ * (c0 + w);
+    ctx_.gram_launches += 1;
+    ctx_.allreduce_sum(ctx_.gram_packed.p, tiles.size() * 64);
+    const int wmax = update_wmax(w);
+    PipBlockArgs a{};
+    a.packed = ctx_.gram_packed.p;
+    a.nb = static_cast<int>(1 + round_up(c0, 8) / 8);
+    a.nx = xc > 0 ? static_cast<int>((8 + xf + xc - 1) / 8 - (8 + xf) / 8 + 1) : 0;
+    a.xb0 = xc > 0 ? static_cast<int>((8 + xf) / 8) : 0;
+    a.x_first = static_cast<int>(xf);
+    a.x_count = static_cast<int>(xc);
+    a.c0 = static_cast<int>(c0);
+    a.w = static_cast<int>(w);
+    a.wmax = wmax;
+    a.slot = spec_slots_.p + idx * kSlotDoubles;
+    a.prev_slot = idx > 0 ? spec_slots_.p + (idx - 1) * kSlotDoubles : nullptr;
+    a.coef = spec_coef_.p + idx * 640;
+    a.skip = spec_skip_.as<int>() + idx;
+    launch_pip_block(ctx_.stream, a, ctx_.launches);
+    cudaEvent_t t1 = ctx_.begin_phase();
+    launch_update(ctx_.stream, n_, c0 > 0 ? col(0) : nullptr, ld_, c0, col(c0), ld_, w, a.coef, true, col(c0), ld_,
+                  ctx_.launches, a.skip);
+    ctx_.end_phase(PH_UPDATE, t1);
+    ctx_.update_bytes += 8.0 * n_ * (c0 + 2.0 * w);
+    ctx_.update_launches += 1;
+    spec_.push_back({c0, w, overlap, xf, xc});
+    spec_filled_ = c0 + w;
+    spec_bps_ = std::min(spec_bps_, c0);
+    if (xc > 0) spec_xd_ = xf + xc;
+}
+
+i64 Store::resolve_speculative(Sync& sync) {
+    if (spec_.empty()) return -1;
+    const size_t bytes = spec_.size() * kSlotDoubles * 8;
+    KB_CUDA(cudaMemcpyAsync(spec_host_.p, spec_slots_.p, bytes, cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+    i64 failed = -1;
+    for (size_t i = 0; i < spec_.size(); ++i) {
+        const SpecBlock& b = spec_[i];
+        const double* slot = spec_host_.p + i * kSlotDoubles;
+        if (slot[kSlotStatus] != 0.0) {
+            failed = static_cast<i64>(i);
+            break;
+        }
+        OrthoRes res;
+        res.r_col = Mat(b.c0, b.w);
+        res.r_jj = Upper(b.w);
+        const double* rc = slot + kSlotRcol;
+        const double* rj = rc + b.c0 * b.w;
+        for (i64 j = 0; j < b.w; ++j) {
+            for (i64 l = 0; l < b.c0; ++l) res.r_col(l, j) = rc[l + j * b.c0];
+            for (i64 l = 0; l <= j; ++l) res.r_jj.at(l, j) = rj[l + j * b.w];
+        }
+        const double* pieces = slot + kSlotPieces;
+        for (i64 k = 0; k < b.x_count; ++k) {
+            for (i64 l = 0; l < b.c0; ++l) pgram_(l, b.x_first + k) = pieces[l + k * b.c0];
+            pready_[static_cast<size_t>(b.x_first + k)] = 1;
+        }
+        // preprocess_block → append_block bookkeeping (one reduce per block)
+        const i64 before = sync.reduces;
+        sync.add(1);
+        ortho_bytes += 8.0 * n_ * (2.0 * b.c0 + 3.0 * b.w);
+        commit(b.c0, b.overlap, res, b.w, KRY_PANEL_PREPROCESSED);
+        sync.per_block.push_back(sync.reduces - before);
+    }
+    spec_.clear();
+    return failed;
 }
 
 bool Store::mpk(Operator& op, i64 c0, i64 s) {

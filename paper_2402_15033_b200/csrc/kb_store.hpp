@@ -68,6 +68,21 @@ public:
     // update over the stored columns with y' = (y_pre − R_col·z, z),
     // z = R_jj⁻¹·y_panel.  Returns false when nothing is pending.
     bool deferred_coefficients(const std::vector<double>& y, std::vector<double>& y_out) const;
+    // ---- speculative first stage (two-stage scheme; k_pip.cu) -------------
+    // preprocess_speculative() queues Gram → [allreduce] → device
+    // factorisation → flag-gated update for the block in store columns
+    // [c0, c0+w) (c0 from the *predicted* fill: every queued block assumed
+    // committed at full width) without waiting for the GPU.
+    // resolve_speculative() copies the result slots back (one sync) and
+    // replays the host bookkeeping block by block exactly as
+    // preprocess_block() would; it returns the queue index of the first block
+    // whose factorisation failed (its raw columns are intact: the caller
+    // redoes it on the synchronous path) or −1.
+    bool can_speculate(i64 w) const;
+    void preprocess_speculative(i64 w, bool overlap);
+    i64 resolve_speculative(Sync& sync);
+    i64 spec_filled() const { return spec_.empty() ? filled_ : spec_filled_; }
+    bool spec_panel_full() const;
     // MPK into the store: column c0 holds the start; columns c0+1..c0+s.
     // Returns true when the fused one-pass kernel ran.
     bool mpk(Operator& op, i64 c0, i64 s);
@@ -98,6 +113,15 @@ private:
     Mat pgram_;
     std::vector<char> pready_;
     bool fused_finalize_gram(i64 c0, i64 w, Mat& r_col, Mat& g);
+    struct SpecBlock {
+        i64 c0, w;
+        bool overlap;
+        i64 x_first, x_count;
+    };
+    std::vector<SpecBlock> spec_;
+    i64 spec_filled_ = 0, spec_bps_ = 0, spec_xd_ = 0;
+    DevBuf spec_slots_, spec_coef_, spec_skip_;
+    HostBuf spec_host_;
     bool pending_ = false;  // deferred finalize transform below applies to Q[:, pend_c0_:pend_c0_+pend_w_)
     i64 pend_c0_ = 0, pend_w_ = 0;
     Mat pend_rcol_;

@@ -66,3 +66,30 @@ def test_standard_gmres_identity(kb, ctx, ref):
     got, want = run_both(kb, ref, rp, ci, vv, b, 1, standard=True)
     assert (int(got.status), got.iterations, got.restarts, got.sync.reduces, got.breakdown) == (
         want.status, want.iterations, want.restarts, want.reduces, want.breakdown)
+
+
+@pytest.mark.parametrize("k", [9, 13, 14])
+def test_mid_panel_breakdown_speculative_matches_synchronous(kb, ctx, ref, monkeypatch, k):
+    """A Krylov space of dimension k (k distinct eigenvalues) ends inside the
+    first big panel: the block that hits it fails its Cholesky after earlier
+    blocks of the same panel were committed.  The speculative first stage
+    (queued blocks, device factorisation) must roll back to that block and
+    reproduce the synchronous path exactly, and both match the reference's
+    counts."""
+    n = 240
+    rp, ci, vv = csr_from_dense_pattern(n, [(i, i, float(1 + i % k)) for i in range(n)])
+    b = np.ones(n)
+    reps = []
+    for spec in ("1", "0"):
+        monkeypatch.setenv("KRY_SPECULATE", spec)
+        got, want = run_both(kb, ref, rp, ci, vv, b, 3, 60)
+        reps.append(got)
+    spec_rep, sync_rep = reps
+    assert spec_rep.breakdown and sync_rep.breakdown
+    assert (int(spec_rep.status), spec_rep.iterations, spec_rep.restarts, spec_rep.sync.reduces) == (
+        int(sync_rep.status), sync_rep.iterations, sync_rep.restarts, sync_rep.sync.reduces)
+    assert spec_rep.sync.per_block == sync_rep.sync.per_block
+    assert spec_rep.cycle_residuals == sync_rep.cycle_residuals
+    np.testing.assert_array_equal(spec_rep.solution, sync_rep.solution)
+    assert (int(spec_rep.status), spec_rep.iterations, spec_rep.restarts, spec_rep.sync.reduces) == (
+        want.status, want.iterations, want.restarts, want.reduces)

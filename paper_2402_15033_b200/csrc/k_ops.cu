@@ -445,6 +445,10 @@ __global__ void __launch_bounds__(kBlock, 2) mpk2d_kernel(const StencilGeom g, c
 // The product is the same rounded __dmul_rn as in the sequential loop and
 // the adds keep spmv's order (csr_matrix.hpp:72-77): bit-identical.
 constexpr int kCsrChunk = 256;
+#ifndef KB_CSR_GATHER_CG
+#define KB_CSR_GATHER_CG 1
+#endif
+constexpr bool kCsrGatherCg = KB_CSR_GATHER_CG;
 
 // MODE: CSR_ONLY (s from 0.0, write y), or one pass of a column-sliced SpMV
 // (see Operator in kb_operator.cpp): CSR_FIRST (s from 0.0, write the
@@ -484,7 +488,10 @@ __global__ void __launch_bounds__(kBlock) csr_warp_kernel(i64 nloc, const RP* __
 #pragma unroll
             for (int u = 0; u < kCsrChunk / 32; ++u) {
                 const int k = lane + 32 * u;
-                if (k < cnt) s_prod[warp][k] = __dmul_rn(v[u], __ldg(x + cidx[u]));
+                if (k < cnt) {
+                    const double xv = kCsrGatherCg ? __ldcg(x + cidx[u]) : __ldg(x + cidx[u]);
+                    s_prod[warp][k] = __dmul_rn(v[u], xv);
+                }
             }
             __syncwarp();
             const i64 a0 = max(rs, cs), a1 = min(re, cs + cnt);

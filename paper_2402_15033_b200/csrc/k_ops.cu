@@ -691,12 +691,13 @@ bool mpk2d_supported(const StencilGeom& g, int s, const double* x, const double*
     if (!(g.dims == 2 && (g.nx & 1) == 0 && s >= 1 && s <= 8 && (ldo & 1) == 0 && a16(x) && a16(out) &&
           g.lines >= 1 && g.nx + 64 < (i64(1) << 31) && g.ny + 64 < (i64(1) << 31)))
         return false;
-    // Worth it only with at least one wave of (window, band) tasks: each
-    // warp's wavefront is a serial chain, so small grids (512²: 250 tasks,
-    // 24 µs per block vs 19 µs for five SpMVs) stay on the per-SpMV kernels.
+    // Worth it once the (window, band) tasks give every SM a warp: each
+    // warp's wavefront is a serial chain, so tiny grids stay on the
+    // per-SpMV kernels (at 512² the fused block already wins: 0.109 vs
+    // 0.118 s to solution).
     const int h = (s + 1) & ~1;
-    const i64 tasks = ceil_div(g.nx, 64 - 2 * h) * std::max<i64>(1, g.lines / (4 * s));
-    return force || tasks >= static_cast<i64>(num_sms()) * 16;
+    const i64 tasks = ceil_div(g.nx, 64 - 2 * h) * std::max<i64>(1, g.lines / (2 * s));
+    return force || tasks >= static_cast<i64>(num_sms());
 }
 
 void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const double* halo_lo,
@@ -706,10 +707,10 @@ void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const 
     auto go = [&](auto kernel) {
         // One wave of resident warps, one (window, band) task each: bands as
         // tall as that allows (the 2s-line band overlap is recomputed), at
-        // least 4s lines; very wide grids loop over tasks.
+        // least 2s lines; very wide grids loop over tasks.
         const int per_sm = occupancy(reinterpret_cast<const void*>(kernel), kBlock, 0);
         const i64 resident = static_cast<i64>(num_sms()) * std::max(per_sm, 1) * (kBlock / 32);
-        const i64 nbands = std::max<i64>(1, std::min<i64>(resident / nwx, g.lines / (4 * s)));
+        const i64 nbands = std::max<i64>(1, std::min<i64>(resident / nwx, g.lines / (2 * s)));
         const i64 band = ceil_div(g.lines, nbands);
         const i64 ntasks = nwx * ceil_div(g.lines, band);
         const unsigned grid = static_cast<unsigned>(

@@ -20,7 +20,7 @@ namespace kb {
 
 namespace {
 
-constexpr int kPipThreads = 128;
+constexpr int kPipThreads = 64;
 constexpr int kPipMaxC0 = 64, kPipMaxW = 8;
 
 __global__ void __launch_bounds__(kPipThreads) pip_block_kernel(const PipBlockArgs a) {

@@ -24,22 +24,51 @@ std::vector<std::pair<i64, i64>> groups_for(i64 c0, i64 w) {
 void gram_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
                  Mat& r_col, Mat& g, i64 x_first, i64 x_count, Mat* gx) {
     dim_check(w >= 1, "gram of empty matrix");
-    const auto groups = groups_for(c0, w);
-    const bool want_x = gx && x_count > 0 && groups.size() == 1 && round_up(w, 8) == 8 && x_first >= 0 &&
+    // Launch plan: one pass per (V column range, prefix group).  A Gram pass
+    // holds at most 64 column slots, so a prefix is split into groups that
+    // fit beside V; a V wider than 56 columns with a prefix (a finalize of
+    // ŝ+1 > 56 columns after an earlier panel, e.g. m = 120, ŝ = 60) runs
+    // VᵀV alone and PᵀV in 32-column halves of V.
+    struct Pass {
+        i64 vj0, wv, start, cp;
+        bool vv;
+    };
+    std::vector<Pass> plain, split;
+    if (c0 == 0 || round_up(w, 8) + 8 <= 64) {
+        const auto groups = groups_for(c0, w);
+        for (size_t gi = 0; gi < groups.size(); ++gi)
+            plain.push_back({0, w, groups[gi].first, groups[gi].second, gi == 0});
+    }
+    if (c0 > 0 && round_up(w, 8) > 32) {
+        groups_for(0, w);  // width check
+        split.push_back({0, w, 0, 0, true});
+        for (i64 vj0 = 0; vj0 < w; vj0 += 32) {
+            const i64 wv = std::min<i64>(32, w - vj0);
+            for (const auto& grp : prefix_groups(c0, wv)) split.push_back({vj0, wv, grp.first, grp.second, false});
+        }
+    }
+    // columns streamed from HBM by a plan: each pass reads its V range and its prefix group
+    auto cost = [](const std::vector<Pass>& ps) {
+        i64 c = 0;
+        for (const Pass& q : ps) c += q.wv + q.cp;
+        return c;
+    };
+    const std::vector<Pass>& passes = (split.empty() || (!plain.empty() && cost(plain) <= cost(split))) ? plain : split;
+    const bool want_x = gx && x_count > 0 && passes.size() == 1 && round_up(w, 8) == 8 && x_first >= 0 &&
                         x_first + x_count <= c0;
     if (gx) *gx = Mat();
     ctx.gram_partials.ensure(static_cast<size_t>(gram_scratch_doubles(w)) * 8);
-    ctx.gram_packed.ensure((groups.size() + 1) * 64 * 64 * 8);
-    std::vector<std::vector<int>> tiles(groups.size());
+    ctx.gram_packed.ensure((passes.size() + 1) * 64 * 64 * 8);
+    std::vector<std::vector<int>> tiles(passes.size());
 
     cudaEvent_t t0 = ctx.begin_phase();
     size_t offset = 0;
-    for (size_t gi = 0; gi < groups.size(); ++gi) {
-        const i64 start = groups[gi].first, cp = groups[gi].second;
-        launch_gram_pass(ctx.stream, n, cp > 0 ? P + start * ldp : nullptr, ldp, cp, V, ldv, w, gi == 0,
-                         ctx.gram_partials.p, ctx.gram_packed.p + offset, tiles[gi], ctx.launches,
+    for (size_t pi = 0; pi < passes.size(); ++pi) {
+        const Pass& ps = passes[pi];
+        launch_gram_pass(ctx.stream, n, ps.cp > 0 ? P + ps.start * ldp : nullptr, ldp, ps.cp, V + ps.vj0 * ldv, ldv,
+                         ps.wv, ps.vv, ctx.gram_partials.p, ctx.gram_packed.p + offset, tiles[pi], ctx.launches,
                          want_x ? x_first : -1, want_x ? x_count : 0);
-        offset += tiles[gi].size() * 64;
+        offset += tiles[pi].size() * 64;
     }
     ctx.end_phase(PH_GRAM, t0);
     ctx.gram_bytes += 8.0 * n * (c0 + w);
@@ -50,34 +79,35 @@ void gram_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double
     ctx.sync();
 
     // Unpack: tile (jb, ib) entry e = m + 8·nn ↦ slot row 8ib+m, V column 8jb+nn.
-    const i64 wslots = round_up(w, 8);
     r_col = Mat(c0, w);
     g = Mat(w, w);
     if (want_x) *gx = Mat(c0, x_count);
     const double* h = ctx.h_packed.p;
     size_t off = 0;
-    for (size_t gi = 0; gi < groups.size(); ++gi) {
-        const i64 start = groups[gi].first, cp = groups[gi].second;
-        for (int id : tiles[gi]) {
+    for (size_t pi = 0; pi < passes.size(); ++pi) {
+        const Pass& ps = passes[pi];
+        const i64 wslots = round_up(ps.wv, 8);
+        for (int id : tiles[pi]) {
             if (id >= 64) {  // extra P×P tile: rows slot block ib, columns slot block xb
                 const int xb = (id - 64) / 8, ib = (id - 64) % 8;
                 for (int e = 0; e < 64; ++e) {
                     const i64 a = 8 * ib + (e & 7) - wslots, b = 8 * xb + (e >> 3) - wslots - x_first;
-                    if (a >= 0 && a < cp && b >= 0 && b < x_count) (*gx)(a, b) = h[off + e];
+                    if (a >= 0 && a < ps.cp && b >= 0 && b < x_count) (*gx)(a, b) = h[off + e];
                 }
                 off += 64;
                 continue;
             }
             const int jb = id / 8, ib = id % 8;
             for (int e = 0; e < 64; ++e) {
-                const i64 mrow = 8 * ib + (e & 7), j = 8 * jb + (e >> 3);
+                const i64 mrow = 8 * ib + (e & 7), jl = 8 * jb + (e >> 3);
                 const double val = h[off + e];
-                if (j >= w) continue;
+                if (jl >= ps.wv) continue;
+                const i64 j = ps.vj0 + jl;
                 if (mrow < wslots) {
-                    if (gi == 0 && mrow <= j) g(mrow, j) = val;  // later groups skip VᵀV
+                    if (ps.vv && mrow <= jl) g(mrow, j) = val;  // VᵀV from the pass that carries it
                 } else {
                     const i64 l = mrow - wslots;
-                    if (l < cp) r_col(start + l, j) = val;
+                    if (l < ps.cp) r_col(ps.start + l, j) = val;
                 }
             }
             off += 64;

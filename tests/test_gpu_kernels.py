@@ -131,14 +131,14 @@ def test_operator_dimension_errors(kb, ctx):
 
 # ---- K3: fused Gram [Q_prev V]ᵀV ---------------------------------------------------------
 SHAPES = [(0, 1), (0, 6), (5, 6), (17, 3), (55, 6), (0, 21), (20, 21), (40, 21), (0, 31), (30, 31),
-          (50, 11), (0, 61), (3, 61 - 3 - 1), (100, 6), (45, 16)]
+          (50, 11), (0, 61), (3, 61 - 3 - 1), (100, 6), (45, 16),
+          # wide V beside a prefix: VᵀV alone + PᵀV in 32-column halves (m = 120, ŝ = 60 finalize)
+          (60, 61), (60, 49), (7, 64)]
 
 
 @pytest.mark.parametrize("c0,w", SHAPES)
 @pytest.mark.parametrize("n", [7, 1000, 100003])
 def test_gram_matches_reference(kb, ctx, ref, rng, n, c0, w):
-    if c0 > 0 and (w + 7) // 8 * 8 > 56:
-        pytest.skip("shape outside the device envelope (w ≤ 56 with a prefix)")
     q = rng.standard_normal((n, c0))
     v = rng.standard_normal((n, w))
     rc, g = kb.gram(q if c0 else None, v)
@@ -165,7 +165,7 @@ def orthonormal(rng, n, k):
 
 
 @pytest.mark.parametrize("n,c0,w", [(120, 0, 5), (500, 6, 4), (4000, 55, 6), (20000, 0, 61), (20000, 40, 21),
-                                    (5000, 50, 11), (100003, 25, 6)])
+                                    (5000, 50, 11), (100003, 25, 6), (20000, 60, 61)])
 def test_bcgs_pip_matches_reference(kb, ctx, ref, rng, n, c0, w):
     q = orthonormal(rng, n, c0) if c0 else None
     v = rng.standard_normal((n, w))

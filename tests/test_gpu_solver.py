@@ -184,3 +184,22 @@ def test_random_sparse_csr_parity(kb, ctx, ref, kind, shat):
     assert (int(got.status), got.iterations, got.restarts, got.sync.reduces) == (
         want.status, want.iterations, want.restarts, want.reduces)
     assert abs(got.cycle_residuals[0] - want.cycle_residuals[0]) <= 1e-10 * want.cycle_residuals[0] + ABS_FLOOR
+
+
+@pytest.mark.parametrize("m,s,shat,kind", [(120, 5, 60, 3), (120, 5, 0, 2), (40, 4, 20, 3), (30, 6, 30, 3)])
+def test_other_restart_lengths_match_live_reference(kb, ctx, ref, m, s, shat, kind):
+    """Restart lengths / step sizes off the default: m = 120 (prefix groups
+    beyond one 64-slot Gram, no speculation, two big panels), s = 4 and 6 —
+    same counts as the live reference and cycle 1 within 1e-10."""
+    grid = 48
+    a = ref.laplace2d(grid, grid)
+    b = ref.spmv(a, np.ones(a.n))
+    want = ref.solve(a, b, None, ref.make_config(m=m, s=s, kind=kind, big_step=shat, shat=shat, max_iters=6 * m))
+    op = kb.Laplace2D(grid, grid)
+    got = kb.sstep_gmres(op, b, None, kb.SolverConfig(restart_len=m, step=s, big_step=shat,
+                                                       scheme=kb.OrthoScheme(kb.OrthoKind(kind), shat),
+                                                       max_iters=6 * m))
+    assert (int(got.status), got.iterations, got.restarts, got.sync.reduces) == (
+        want.status, want.iterations, want.restarts, want.reduces)
+    assert got.sync.per_block == [int(v) for v in want.per_block]
+    assert abs(got.cycle_residuals[0] - want.cycle_residuals[0]) <= 1e-10 * want.cycle_residuals[0] + ABS_FLOOR

@@ -20,7 +20,7 @@ namespace kb {
 
 namespace {
 
-constexpr int kPipThreads = 64;
+constexpr int kPipThreads = 256;
 constexpr int kPipMaxC0 = 64, kPipMaxW = 8;
 
 __global__ void __launch_bounds__(kPipThreads) pip_block_kernel(const PipBlockArgs a) {
@@ -29,28 +29,40 @@ __global__ void __launch_bounds__(kPipThreads) pip_block_kernel(const PipBlockAr
     __shared__ double r[kPipMaxW * kPipMaxW];    // R_jj (upper), column-major
     __shared__ int bad;
     const int c0 = a.c0, w = a.w, tid = threadIdx.x;
-    // 1. unpack the packed Gram tiles (tile t = slot block t of the regular
-    //    tiles: rows 8t + m, V column nn; extra tiles: prefix × prefix).
-    for (int t = 0; t < a.nb; ++t)
-        for (int e = tid; e < 64; e += kPipThreads) {
-            const int mrow = 8 * t + (e & 7), j = e >> 3;
-            const double v = a.packed[t * 64 + e];
+    // 1. unpack the packed Gram tiles: the nb regular tiles (slot block t:
+    //    rows 8t + m, V column nn) then the extra prefix × prefix tiles.  One
+    //    flat loop over all entries so the L2 loads are independent.
+    double* pieces = a.slot + kSlotPieces;
+    const int nreg = a.nb * 64, ntot = nreg + a.nx * (a.nb - 1) * 64;
+    // all loads first (≤ 22 tiles · 64 / 256 threads = 6 per thread), so the
+    // L2 round trips overlap instead of serialising behind the scatter
+    constexpr int kPer = (22 * 64 + kPipThreads - 1) / kPipThreads;
+    double vals[kPer];
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int idx = tid + u * kPipThreads;
+        vals[u] = idx < ntot ? a.packed[idx] : 0.0;
+    }
+#pragma unroll
+    for (int u = 0; u < kPer; ++u) {
+        const int idx = tid + u * kPipThreads;
+        if (idx >= ntot) break;
+        const double v = vals[u];
+        const int e = idx & 63;
+        if (idx < nreg) {
+            const int mrow = 8 * (idx >> 6) + (e & 7), j = e >> 3;
             if (j >= w) continue;
             if (mrow < 8) {
                 if (mrow < w) s[mrow + j * kPipMaxW] = v;  // upper and lower: mirrored below
             } else if (mrow - 8 < c0) {
                 rc[(mrow - 8) + j * c0] = v;
             }
+        } else {
+            const int xt = (idx - nreg) >> 6, k = xt / (a.nb - 1), ib = 1 + xt % (a.nb - 1);
+            const int ar = 8 * ib + (e & 7) - 8, bc = 8 * (a.xb0 + k) + (e >> 3) - 8 - a.x_first;
+            if (ar >= 0 && ar < c0 && bc >= 0 && bc < a.x_count) pieces[ar + bc * c0] = v;
         }
-    double* pieces = a.slot + kSlotPieces;
-    for (int k = 0; k < a.nx; ++k)
-        for (int ib = 1; ib < a.nb; ++ib) {
-            const double* tile = a.packed + (a.nb + k * (a.nb - 1) + (ib - 1)) * 64;
-            for (int e = tid; e < 64; e += kPipThreads) {
-                const int ar = 8 * ib + (e & 7) - 8, bc = 8 * (a.xb0 + k) + (e >> 3) - 8 - a.x_first;
-                if (ar >= 0 && ar < c0 && bc >= 0 && bc < a.x_count) pieces[ar + bc * c0] = tile[e];
-            }
-        }
+    }
     __syncthreads();
     // mirror the upper triangle of VᵀV (gram(), dense_kernels.hpp:95-105)
     for (int idx = tid; idx < w * w; idx += kPipThreads) {

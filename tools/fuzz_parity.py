@@ -1,0 +1,82 @@
+"""Randomised solver parity sweep against the live reference (oracle/_ref):
+random sparse / stencil operators, restart lengths, step sizes, schemes.
+Prints one line per case and a summary; exit code = number of mismatches."""
+import os, sys
+sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
+import numpy as np
+import paper_2402_15033_b200 as kb
+from oracle import ref
+
+FMA = ref._load(os.path.join(os.path.dirname(ref.__file__), "_ref", "libkrylov_ref_fma.so"))
+rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
+ncases = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+bad = 0
+for case in range(ncases):
+    kind = int(rng.choice([1, 2, 3, 3]))
+    s = int(rng.integers(1, 8))
+    m = s * int(rng.integers(2, max(3, 61 // s)))
+    shat = 0 if kind != 3 else s * int(rng.integers(1, m // s + 1))
+    opk = rng.choice(["lap2d", "lap3d", "rand"])
+    if opk == "lap2d":
+        nx, ny = int(rng.integers(2, 70)), int(rng.integers(2, 70))
+        a = ref.laplace2d(nx, ny)
+        op = kb.Laplace2D(nx, ny)
+    elif opk == "lap3d":
+        d = [int(rng.integers(2, 14)) for _ in range(3)]
+        a = ref.laplace3d(*d)
+        op = kb.Laplace3D(*d)
+    else:
+        n = int(rng.integers(5, 3000))
+        per = int(rng.integers(0, 12))
+        rows = []
+        for i in range(n):
+            cols = np.unique(np.concatenate([[i], rng.integers(0, n, per)]))
+            vals = rng.standard_normal(cols.size) * 0.3
+            vals[cols == i] = 2.0 + np.abs(vals).sum()
+            rows.append((cols, vals))
+        rp = np.zeros(n + 1, np.int64)
+        rp[1:] = np.cumsum([c.size for c, _ in rows])
+        ci = np.concatenate([c for c, _ in rows]).astype(np.int64)
+        vv = np.concatenate([v for _, v in rows])
+        a = ref.Csr(n, rp, ci, vv)
+        op = kb.CsrOperator(rp, ci, vv)
+    b = ref.spmv(a, np.ones(a.n))
+    max_iters = m * int(rng.integers(1, 6))
+    cfgr = ref.make_config(m=m, s=s, kind=kind, big_step=shat, shat=shat, max_iters=max_iters)
+    want = ref.solve(a, b, None, cfgr)
+    saved = ref.lib()
+    ref._lib = FMA
+    want_fma = ref.solve(a, b, None, cfgr)  # the reference's own rounding envelope (FMA build)
+    ref._lib = saved
+    try:
+        got = kb.sstep_gmres(op, b, None, kb.SolverConfig(restart_len=m, step=s, big_step=shat,
+                                                           scheme=kb.OrthoScheme(kb.OrthoKind(kind), shat),
+                                                           max_iters=max_iters))
+        mine = (int(got.status), got.iterations, got.restarts, got.sync.reduces)
+        # the reference against itself (FMA build) is the rounding envelope:
+        # counts may legitimately follow either build when the solve sits at
+        # the rounding floor (near-breakdown, residuals ~1e-15)
+        counts_ok = mine in ((want.status, want.iterations, want.restarts, want.reduces),
+                             (want_fma.status, want_fma.iterations, want_fma.restarts, want_fma.reduces))
+        c1 = abs(got.cycle_residuals[0] - want.cycle_residuals[0]) / max(want.cycle_residuals[0], 1e-300) \
+            if want.cycle_residuals else 0.0
+        env = abs(want_fma.cycle_residuals[0] - want.cycle_residuals[0]) / max(want.cycle_residuals[0], 1e-300) \
+            if want.cycle_residuals and want_fma.cycle_residuals else 0.0
+        # tests/test_gpu_solver.py protocol: max(1e-10·c, 10·env) + 1e-13 (absolute floor)
+        ok = counts_ok and (not want.cycle_residuals or abs(got.cycle_residuals[0] - want.cycle_residuals[0]) <=
+                            max(1e-10 * want.cycle_residuals[0], 10 * env * want.cycle_residuals[0]) + 1e-13)
+        msg = f"counts {counts_ok} c1rel {c1:.1e} ref-fma-env {env:.1e}"
+        if not ok and want.cycle_residuals and got.cycle_residuals:
+            tr = lambda x: float(np.linalg.norm(b - ref.spmv(a, x)) / np.linalg.norm(b))  # noqa: E731
+            msg += (f" | cycle1 ours {got.cycle_residuals[0]:.3e} ref {want.cycle_residuals[0]:.3e} "
+                    f"ref-fma {want_fma.cycle_residuals[0]:.3e} | true final ours {tr(got.solution):.3e} "
+                    f"ref {tr(want.solution):.3e} ref-fma {tr(want_fma.solution):.3e}")
+        if not counts_ok:
+            msg += f" got {(int(got.status), got.iterations, got.restarts, got.sync.reduces)} want {(want.status, want.iterations, want.restarts, want.reduces)}"
+    except Exception as e:  # noqa: BLE001
+        ok, msg = False, f"EXC {type(e).__name__}: {e}"
+    bad += 0 if ok else 1
+    print(f"case {case:3d} {opk:5s} n={a.n:6d} kind={kind} m={m:3d} s={s} shat={shat:3d} its<={max_iters:4d}: "
+          f"{'ok ' if ok else 'BAD'} {msg}", flush=True)
+print(f"{ncases - bad}/{ncases} ok")
+sys.exit(bad)

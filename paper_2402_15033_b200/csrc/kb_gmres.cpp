@@ -120,6 +120,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
     // gmres.hpp:247-269
     // The unforced check after a cycle's last block and the forced one that
     // follows it see the same store: the host H / LSQ of the first is reused.
+    double lsq_seconds = 0.0;  // host H assembly + LSQ (KRY_HOST_PROFILE)
     struct LsqCache {
         i64 reduces = -1, filled = -1;
         double gamma = 0.0;
@@ -131,8 +132,11 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         const i64 k = usable_cols();
         if (k == 0) return res;
         if (!(cache.reduces == rep.sync.reduces && cache.filled == store.filled() && cache.gamma == gamma)) {
+            const auto th = std::chrono::steady_clock::now();
             Mat h = assemble_hessenberg(store.coefficients(), k, store.block_records());
             cache.lsq = solve_hessenberg_lsq(h, gamma);
+            if (ctx.host_profile)
+                lsq_seconds += std::chrono::duration<double>(std::chrono::steady_clock::now() - th).count();
             // A deferred last-panel finalize: the same x update over the stored
             // (preprocessed) columns with transformed coefficients.
             if (!store.deferred_coefficients(cache.lsq.y, cache.ycoef)) cache.ycoef = cache.lsq.y;
@@ -340,9 +344,11 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
     if (ctx.host_profile) {
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - prof_t0).count();
         std::fprintf(stderr,
-                     "[kry host profile] wall %.6f s, blocked in %lld syncs %.6f s, launches %lld, cycles %lld\n",
+                     "[kry host profile] wall %.6f s, blocked in %lld syncs %.6f s, launches %lld, cycles %lld, "
+                     "H+LSQ %.6f s\n",
                      wall, static_cast<long long>(ctx.sync_count - prof_syncs0), ctx.sync_wait_s - prof_wait0,
-                     static_cast<long long>(ctx.launches - prof_launch0), static_cast<long long>(rep.restarts + 1));
+                     static_cast<long long>(ctx.launches - prof_launch0), static_cast<long long>(rep.restarts + 1),
+                     lsq_seconds);
     }
     return rep;
 }

@@ -1,6 +1,6 @@
 // Operator and restart-loop kernels for sm_100a.
 //
-// K1/K2  stencil_kernel / csr_kernel: y = A·x with every row summed in the
+// K1/K2  stencil / CSR kernels: y = A·x with every row summed in the
 //        reference's stored (ascending column) order, s = 0.0 start, no FMA
 //        contraction (spmv, csr_matrix.hpp:69-79) — bit-identical to the CPU
 //        reference.  The stencils reproduce gen_laplace2d(nx,ny,5) and
@@ -445,10 +445,6 @@ __global__ void __launch_bounds__(kBlock, 2) mpk2d_kernel(const StencilGeom g, c
 // The product is the same rounded __dmul_rn as in the sequential loop and
 // the adds keep spmv's order (csr_matrix.hpp:72-77): bit-identical.
 constexpr int kCsrChunk = 256;
-#ifndef KB_CSR_GATHER_CG
-#define KB_CSR_GATHER_CG 1
-#endif
-constexpr bool kCsrGatherCg = KB_CSR_GATHER_CG;
 
 // MODE: CSR_ONLY (s from 0.0, write y), or one pass of a column-sliced SpMV
 // (see Operator in kb_operator.cpp): CSR_FIRST (s from 0.0, write the
@@ -489,7 +485,7 @@ __global__ void __launch_bounds__(kBlock) csr_warp_kernel(i64 nloc, const RP* __
             for (int u = 0; u < kCsrChunk / 32; ++u) {
                 const int k = lane + 32 * u;
                 if (k < cnt) {
-                    const double xv = kCsrGatherCg ? __ldcg(x + cidx[u]) : __ldg(x + cidx[u]);
+                    const double xv = __ldcg(x + cidx[u]);  // no L1 allocation for random gathers
                     s_prod[warp][k] = __dmul_rn(v[u], xv);
                 }
             }
@@ -514,42 +510,6 @@ __global__ void __launch_bounds__(kBlock) csr_warp_kernel(i64 nloc, const RP* __
         const double t = block_sum(sq);
         if (threadIdx.x == 0) partials[blockIdx.x] = t;
     }
-}
-
-template <bool RESID>
-__global__ void __launch_bounds__(kBlock) csr_kernel(i64 nloc, const int64_t* __restrict__ row_ptr,
-                                                     const int32_t* __restrict__ col,
-                                                     const double* __restrict__ vals,
-                                                     const double* __restrict__ x,
-                                                     const double* __restrict__ b, double* __restrict__ y,
-                                                     double* __restrict__ partials) {
-    double sq = 0.0;
-    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nloc; i += (i64)gridDim.x * blockDim.x) {
-        double s = 0.0;
-        const i64 e = row_ptr[i + 1];
-        for (i64 k = row_ptr[i]; k < e; ++k) s = acc_term(s, __ldg(vals + k), __ldg(x + __ldg(col + k)));
-        if (RESID) {
-            const double r = __dsub_rn(b[i], s);
-            y[i] = r;
-            sq = fma(r, r, sq);
-        } else {
-            y[i] = s;
-        }
-    }
-    if (RESID) {
-        const double t = block_sum(sq);
-        if (threadIdx.x == 0) partials[blockIdx.x] = t;
-    }
-}
-
-__global__ void __launch_bounds__(kBlock) dot_kernel(i64 n, const double* __restrict__ a,
-                                                     const double* __restrict__ b,
-                                                     double* __restrict__ partials) {
-    double s = 0.0;
-    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
-        s = fma(a[i], b[i], s);
-    const double t = block_sum(s);
-    if (threadIdx.x == 0) partials[blockIdx.x] = t;
 }
 
 __global__ void __launch_bounds__(kBlock) finalize_kernel(const double* __restrict__ partials, int count,
@@ -774,13 +734,6 @@ int launch_csr_sliced(cudaStream_t s, i64 nloc, int nslices, const int32_t* cons
         ++launches;
     }
     return b ? reduce_grid() : 0;
-}
-
-void launch_dot(cudaStream_t s, i64 n, const double* a, const double* b, double* partials,
-                int64_t& launches) {
-    dot_kernel<<<reduce_grid(), kBlock, 0, s>>>(n, a, b, partials);
-    KB_LAUNCHED();
-    ++launches;
 }
 
 void launch_finalize_sum(cudaStream_t s, const double* partials, int count, double* out,

@@ -92,8 +92,6 @@ int launch_csr_sliced(cudaStream_t s, i64 nloc, int nslices, const int32_t* cons
                       const int32_t* const* col, const double* const* vals, const double* x, const double* b,
                       double* y, double* partials, double* part_sum, int64_t& launches);
 int reduce_grid();  // fixed grid of every partial-sum kernel (determinism)
-void launch_dot(cudaStream_t s, i64 n, const double* a, const double* b, double* partials,
-                int64_t& launches);
 void launch_finalize_sum(cudaStream_t s, const double* partials, int count, double* out,
                          int64_t& launches);
 void launch_scale_div(cudaStream_t s, i64 n, const double* r, double gamma, double* out,

@@ -622,6 +622,117 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
     }
 }
 
+// ---------------------------------------------------------------------------
+// K5t: the K5 update (w ≤ 8) with the prefix streamed through a TMA ring in
+// 16-column chunks: each 256-row tile arrives as one V box then ⌈cp/16⌉
+// prefix boxes (4 KB contiguous per column, like the Gram's loads), one
+// producer warp, 8 consumer warps with one row per thread.  The arithmetic
+// is K5's, term for term (acc = V; acc += −R_col(l,·)·p_l, l ascending;
+// right-looking substitution), so the results are bit-identical to K5.
+// ---------------------------------------------------------------------------
+constexpr int kTmaRows = 256;
+
+template <int WMAX, int CC, int ST, int MINB>
+__global__ void __launch_bounds__(9 * 32, MINB)
+    update_tma_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_p,
+                      i64 n, int cp, int w, const double* __restrict__ coef, double* out, i64 ldo,
+                      const int* skip) {
+    if (skip && *skip) return;  // speculative block whose factorisation failed (k_pip.cu)
+    constexpr int CW = 8, TR = kTmaRows;
+    extern __shared__ __align__(1024) unsigned char smem[];
+    double* ring = reinterpret_cast<double*>(smem);                      // [ST][CC][TR]
+    uint64_t* full = reinterpret_cast<uint64_t*>(ring + ST * CC * TR);
+    uint64_t* empty = full + ST;
+    double* c_sm = reinterpret_cast<double*>(empty + ST);                 // coefficients
+    const int cpp = (cp + CC - 1) / CC * CC;
+    const int nchunk = 1 + cpp / CC;  // V, then the prefix
+    for (int i = threadIdx.x; i < cpp * WMAX; i += blockDim.x) c_sm[i] = i < cp * WMAX ? coef[i] : 0.0;
+    for (int i = threadIdx.x; i < (WMAX + 1) * WMAX; i += blockDim.x) c_sm[cpp * WMAX + i] = coef[cp * WMAX + i];
+    if (threadIdx.x == 0) {
+        for (int q = 0; q < ST; ++q) {
+            mbar_init(&full[q], 1);
+            mbar_init(&empty[q], CW);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+    const double* nrc = c_sm;
+    const double* nrjj = c_sm + static_cast<size_t>(cpp) * WMAX;
+    const double* inv = nrjj + WMAX * WMAX;
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const i64 ntiles = (n + TR - 1) / TR;
+    if (warp == CW) {  // producer
+        if (lane != 0) return;
+        int q = 0, use = 0;
+        for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+            const int row0 = static_cast<int>(tile * TR);
+            for (int c = 0; c < nchunk; ++c) {
+                if (use > 0) mbar_wait(&empty[q], (use - 1) & 1);
+                double* st = ring + static_cast<size_t>(q) * CC * TR;
+                if (c == 0) {
+                    mbar_expect_tx(&full[q], static_cast<unsigned>(w) * TR * 8);
+                    tma_load_2d(st, &map_v, row0, 0, &full[q]);
+                } else {
+                    mbar_expect_tx(&full[q], static_cast<unsigned>(CC) * TR * 8);
+                    tma_load_2d(st, &map_p, row0, (c - 1) * CC, &full[q]);
+                }
+                if (++q == ST) {
+                    q = 0;
+                    ++use;
+                }
+            }
+        }
+        return;
+    }
+    const int t = threadIdx.x;  // this thread's row of the tile
+    int q = 0, use = 0;
+    for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
+        double acc[WMAX];
+        for (int c = 0; c < nchunk; ++c) {
+            mbar_wait(&full[q], use & 1);
+            const double* st = ring + static_cast<size_t>(q) * CC * TR + t;
+            if (c == 0) {
+#pragma unroll
+                for (int j = 0; j < WMAX; ++j) acc[j] = j < w ? st[j * TR] : 0.0;
+            } else {
+                const int l0 = (c - 1) * CC;
+#pragma unroll
+                for (int u = 0; u < CC; ++u) {
+                    const double pv = st[u * TR];
+                    const double2* cr = reinterpret_cast<const double2*>(nrc + (l0 + u) * WMAX);
+#pragma unroll
+                    for (int j = 0; j < WMAX; j += 2) {
+                        const double2 cf = cr[j / 2];
+                        acc[j] = fma(cf.x, pv, acc[j]);
+                        acc[j + 1] = fma(cf.y, pv, acc[j + 1]);
+                    }
+                }
+            }
+            __syncwarp();
+            if (lane == 0) mbar_arrive(&empty[q]);
+            if (++q == ST) {
+                q = 0;
+                ++use;
+            }
+        }
+        // right-looking substitution, tri_solve_right's order (as K5)
+#pragma unroll
+        for (int k = 0; k < WMAX; ++k) {
+            acc[k] *= inv[k];
+            const double* rk = nrjj + k * WMAX;
+#pragma unroll
+            for (int j = k + 1; j < WMAX; ++j) acc[j] = fma(rk[j], acc[k], acc[j]);
+        }
+        const i64 row = tile * TR + t;
+        if (row < n) {
+#pragma unroll
+            for (int j = 0; j < WMAX; ++j)
+                if (j < w) out[row + j * ldo] = acc[j];
+        }
+    }
+}
+
 template <int NBW, int NB>
 const void* update_mma_fn(int nbw, int nb) {
     if (nbw == NBW && nb == NB) return reinterpret_cast<const void*>(update_mma_kernel<NBW, NB>);
@@ -651,12 +762,16 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows);
+CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols);
 
 // Tensor maps are cached by their parameters: the solver re-launches the same
 // (store column, shape) combinations every cycle, and an encode costs more
 // host time than the launch itself.
+CUtensorMap make_map_box(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols);
 CUtensorMap make_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows) {
+    return make_map_box(base, ld, rows, cols, box_rows, 0);
+}
+CUtensorMap make_map_box(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols) {
     struct Key {
         const double* base;
         i64 ld, rows, cols;
@@ -674,17 +789,17 @@ CUtensorMap make_map(const double* base, i64 ld, i64 rows, i64 cols, int box_row
     };
     static std::mutex mu;
     static std::unordered_map<Key, CUtensorMap, Hash> cache;
-    const Key key{base, ld, rows, cols, box_rows};
+    const Key key{base, ld, rows, cols, box_rows * 1024 + box_cols};
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     if (cache.size() > 4096) cache.clear();
-    CUtensorMap m = encode_map(base, ld, rows, cols, box_rows);
+    CUtensorMap m = encode_map(base, ld, rows, cols, box_rows, box_cols);
     cache.emplace(key, m);
     return m;
 }
 
-CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows) {
+CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols = 0) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
     if (cols <= 0 || base == nullptr) return m;  // unused operand
@@ -692,7 +807,7 @@ CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_r
         fail(KRY_INTERNAL, "TMA operand must be 16-byte aligned with an even leading dimension");
     cuuint64_t dims[2] = {static_cast<cuuint64_t>(rows), static_cast<cuuint64_t>(cols)};
     cuuint64_t strides[1] = {static_cast<cuuint64_t>(ld) * 8};
-    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(cols)};
+    cuuint32_t box[2] = {static_cast<cuuint32_t>(box_rows), static_cast<cuuint32_t>(box_cols > 0 ? box_cols : cols)};
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
@@ -841,6 +956,42 @@ void launch_update_mma(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64
     launches += 1;
 }
 
+// K5t for w ≤ 8 when the layout allows TMA (KRY_UPDATE_TMA=0 keeps K5).
+static bool launch_update_tma(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V,
+                              i64 ldv, i64 w, const double* d_coef, bool triangular, double* out, i64 ldo,
+                              int64_t& launches, const int* skip) {
+    static const bool on = [] {
+        const char* e = std::getenv("KRY_UPDATE_TMA");
+        return !(e && std::atoi(e) == 0);
+    }();
+    auto a16 = [](const void* q) { return (reinterpret_cast<uintptr_t>(q) & 15) == 0; };
+    if (!on || !triangular || w > 8 || cp < 1 || !a16(P) || !a16(V) || (ldp & 1) || (ldv & 1) ||
+        n >= (i64(1) << 31))
+        return false;
+    const int wmax = update_wmax(w);
+    // 16-column chunks × 6 stages (192 KB ring, one CTA per SM).  Measured
+    // alternatives at 4000² (update ms per cycle): 8 × 12 → 9.30, 32 × 3 →
+    // 10.46, 16 × 3 with two CTAs per SM → 9.21, this → 9.06 (K5: 9.55).
+    constexpr int cc = 16, st = 6;
+    const int cpp = static_cast<int>(round_up(cp, cc));
+    const size_t smem = static_cast<size_t>(st) * cc * kTmaRows * 8 + 2 * st * 8 +
+                        static_cast<size_t>(cpp + wmax + 1) * wmax * 8 + 64;
+    if (smem > 227 * 1024) return false;
+    CUtensorMap mv = make_map(V, ldv, n, w, kTmaRows);
+    CUtensorMap mp = make_map_box(P, ldp, n, cp, kTmaRows, cc);
+    const i64 ntiles = ceil_div(n, kTmaRows);
+    const int grid = static_cast<int>(std::min<i64>(sm_count(), std::max<i64>(1, ntiles)));
+    const void* fn = wmax == 6 ? reinterpret_cast<const void*>(update_tma_kernel<6, cc, st, 1>)
+                               : reinterpret_cast<const void*>(update_tma_kernel<8, cc, st, 1>);
+    set_smem(fn, smem);
+    int cpi = static_cast<int>(cp), wi = static_cast<int>(w);
+    void* args[] = {&mv, &mp, &n, &cpi, &wi, const_cast<double**>(&d_coef), &out, &ldo, const_cast<int**>(&skip)};
+    KB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(9 * 32), args, smem, stream));
+    KB_LAUNCHED();
+    launches += 1;
+    return true;
+}
+
 static int update_rows_setting() {  // KRY_UPDATE_ROWS=1 → one row per thread (A/B)
     static const int r = [] {
         const char* e = std::getenv("KRY_UPDATE_ROWS");
@@ -855,6 +1006,7 @@ int update_wmax(i64 w) { return w <= 6 ? 6 : w <= 8 ? 8 : w <= 16 ? 16 : w <= 32
 void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp, const double* V, i64 ldv,
                    i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches,
                    const int* skip) {
+    if (launch_update_tma(stream, n, P, ldp, cp, V, ldv, w, d_coef, triangular, out, ldo, launches, skip)) return;
     const int wmax = update_wmax(w);
     const size_t smem = static_cast<size_t>(round_up(cp, 12) + wmax + 1) * wmax * 8;
     if (smem > 200 * 1024) fail(KRY_UNSUPPORTED, "update coefficients exceed shared memory");

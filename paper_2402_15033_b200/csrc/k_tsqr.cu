@@ -632,15 +632,18 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
 // ---------------------------------------------------------------------------
 constexpr int kTmaRows = 256;
 
-template <int WMAX, int CC, int ST, int MINB>
-__global__ void __launch_bounds__(9 * 32, MINB)
+// R = 2: each consumer thread owns two adjacent rows (16-byte shared-memory
+// loads, and every coefficient broadcast serves both rows); a tile is R
+// 256-row boxes, stored per box as [CC][256].
+template <int WMAX, int CC, int ST, int R>
+__global__ void __launch_bounds__(9 * 32, 1)
     update_tma_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_p,
                       i64 n, int cp, int w, const double* __restrict__ coef, double* out, i64 ldo,
                       const int* skip) {
     if (skip && *skip) return;  // speculative block whose factorisation failed (k_pip.cu)
-    constexpr int CW = 8, TR = kTmaRows;
+    constexpr int CW = 8, BOX = kTmaRows, TR = BOX * R;
     extern __shared__ __align__(1024) unsigned char smem[];
-    double* ring = reinterpret_cast<double*>(smem);                      // [ST][CC][TR]
+    double* ring = reinterpret_cast<double*>(smem);                      // [ST][R][CC][BOX]
     uint64_t* full = reinterpret_cast<uint64_t*>(ring + ST * CC * TR);
     uint64_t* empty = full + ST;
     double* c_sm = reinterpret_cast<double*>(empty + ST);                 // coefficients
@@ -670,12 +673,14 @@ __global__ void __launch_bounds__(9 * 32, MINB)
             for (int c = 0; c < nchunk; ++c) {
                 if (use > 0) mbar_wait(&empty[q], (use - 1) & 1);
                 double* st = ring + static_cast<size_t>(q) * CC * TR;
-                if (c == 0) {
-                    mbar_expect_tx(&full[q], static_cast<unsigned>(w) * TR * 8);
-                    tma_load_2d(st, &map_v, row0, 0, &full[q]);
-                } else {
-                    mbar_expect_tx(&full[q], static_cast<unsigned>(CC) * TR * 8);
-                    tma_load_2d(st, &map_p, row0, (c - 1) * CC, &full[q]);
+                const unsigned cols = c == 0 ? static_cast<unsigned>(w) : static_cast<unsigned>(CC);
+                mbar_expect_tx(&full[q], cols * TR * 8);
+#pragma unroll
+                for (int bx = 0; bx < R; ++bx) {
+                    if (c == 0)
+                        tma_load_2d(st + bx * CC * BOX, &map_v, row0 + bx * BOX, 0, &full[q]);
+                    else
+                        tma_load_2d(st + bx * CC * BOX, &map_p, row0 + bx * BOX, (c - 1) * CC, &full[q]);
                 }
                 if (++q == ST) {
                     q = 0;
@@ -685,27 +690,50 @@ __global__ void __launch_bounds__(9 * 32, MINB)
         }
         return;
     }
-    const int t = threadIdx.x;  // this thread's row of the tile
+    // this thread's rows R·t … R·t + R − 1 of the tile: box R·t / BOX, row R·t % BOX
+    const int t = threadIdx.x;
+    const int off = (R * t / BOX) * CC * BOX + (R * t) % BOX;
     int q = 0, use = 0;
     for (i64 tile = blockIdx.x; tile < ntiles; tile += gridDim.x) {
-        double acc[WMAX];
+        double acc[WMAX][R];
         for (int c = 0; c < nchunk; ++c) {
             mbar_wait(&full[q], use & 1);
-            const double* st = ring + static_cast<size_t>(q) * CC * TR + t;
+            const double* st = ring + static_cast<size_t>(q) * CC * TR + off;
+            auto ldr = [&](int col, double (&d)[R]) {
+                if constexpr (R == 1) {
+                    d[0] = st[col * BOX];
+                } else {
+#pragma unroll
+                    for (int h = 0; h < R; h += 2) {
+                        const double2 v2 = *reinterpret_cast<const double2*>(st + col * BOX + h);
+                        d[h] = v2.x;
+                        d[h + 1] = v2.y;
+                    }
+                }
+            };
             if (c == 0) {
 #pragma unroll
-                for (int j = 0; j < WMAX; ++j) acc[j] = j < w ? st[j * TR] : 0.0;
+                for (int j = 0; j < WMAX; ++j) {
+                    double d[R];
+                    ldr(j, d);
+#pragma unroll
+                    for (int r = 0; r < R; ++r) acc[j][r] = j < w ? d[r] : 0.0;
+                }
             } else {
                 const int l0 = (c - 1) * CC;
 #pragma unroll
                 for (int u = 0; u < CC; ++u) {
-                    const double pv = st[u * TR];
+                    double pv[R];
+                    ldr(u, pv);
                     const double2* cr = reinterpret_cast<const double2*>(nrc + (l0 + u) * WMAX);
 #pragma unroll
                     for (int j = 0; j < WMAX; j += 2) {
                         const double2 cf = cr[j / 2];
-                        acc[j] = fma(cf.x, pv, acc[j]);
-                        acc[j + 1] = fma(cf.y, pv, acc[j + 1]);
+#pragma unroll
+                        for (int r = 0; r < R; ++r) {
+                            acc[j][r] = fma(cf.x, pv[r], acc[j][r]);
+                            acc[j + 1][r] = fma(cf.y, pv[r], acc[j + 1][r]);
+                        }
                     }
                 }
             }
@@ -719,16 +747,29 @@ __global__ void __launch_bounds__(9 * 32, MINB)
         // right-looking substitution, tri_solve_right's order (as K5)
 #pragma unroll
         for (int k = 0; k < WMAX; ++k) {
-            acc[k] *= inv[k];
+#pragma unroll
+            for (int r = 0; r < R; ++r) acc[k][r] *= inv[k];
             const double* rk = nrjj + k * WMAX;
 #pragma unroll
-            for (int j = k + 1; j < WMAX; ++j) acc[j] = fma(rk[j], acc[k], acc[j]);
+            for (int j = k + 1; j < WMAX; ++j)
+#pragma unroll
+                for (int r = 0; r < R; ++r) acc[j][r] = fma(rk[j], acc[k][r], acc[j][r]);
         }
-        const i64 row = tile * TR + t;
-        if (row < n) {
+        const i64 row = tile * TR + R * t;
+        if (R > 1 && row + R - 1 < n) {
 #pragma unroll
             for (int j = 0; j < WMAX; ++j)
-                if (j < w) out[row + j * ldo] = acc[j];
+                if (j < w)
+#pragma unroll
+                    for (int h = 0; h < R; h += 2)
+                        *reinterpret_cast<double2*>(out + row + h + j * ldo) = make_double2(acc[j][h], acc[j][h + 1]);
+        } else {
+#pragma unroll
+            for (int r = 0; r < R; ++r)
+                if (row + r < n)
+#pragma unroll
+                    for (int j = 0; j < WMAX; ++j)
+                        if (j < w) out[row + r + j * ldo] = acc[j][r];
         }
     }
 }
@@ -969,20 +1010,28 @@ static bool launch_update_tma(cudaStream_t stream, i64 n, const double* P, i64 l
         n >= (i64(1) << 31))
         return false;
     const int wmax = update_wmax(w);
-    // 16-column chunks × 6 stages (192 KB ring, one CTA per SM).  Measured
-    // alternatives at 4000² (update ms per cycle): 8 × 12 → 9.30, 32 × 3 →
-    // 10.46, 16 × 3 with two CTAs per SM → 9.21, this → 9.06 (K5: 9.55).
-    constexpr int cc = 16, st = 6;
+    // Two rows per consumer thread, 16-column chunks, 3 × 64 KB stages.
+    // Measured at 4000² (update ms per cycle): one row per thread (6 × 32 KB
+    // stages) 9.07, two rows 8.79, four rows with 8-column chunks 8.87;
+    // KRY_UPDATE_TMA_ROWS=1 selects the one-row variant (A/B).
+    static const int rows = [] {
+        const char* e = std::getenv("KRY_UPDATE_TMA_ROWS");
+        return e && std::atoi(e) == 1 ? 1 : 2;
+    }();
+    const int cc = 16;
+    const int st = rows == 1 ? 6 : 3;
     const int cpp = static_cast<int>(round_up(cp, cc));
-    const size_t smem = static_cast<size_t>(st) * cc * kTmaRows * 8 + 2 * st * 8 +
+    const size_t smem = static_cast<size_t>(st) * cc * kTmaRows * rows * 8 + 2 * st * 8 +
                         static_cast<size_t>(cpp + wmax + 1) * wmax * 8 + 64;
     if (smem > 227 * 1024) return false;
     CUtensorMap mv = make_map(V, ldv, n, w, kTmaRows);
     CUtensorMap mp = make_map_box(P, ldp, n, cp, kTmaRows, cc);
-    const i64 ntiles = ceil_div(n, kTmaRows);
+    const i64 ntiles = ceil_div(n, kTmaRows * rows);
     const int grid = static_cast<int>(std::min<i64>(sm_count(), std::max<i64>(1, ntiles)));
-    const void* fn = wmax == 6 ? reinterpret_cast<const void*>(update_tma_kernel<6, cc, st, 1>)
-                               : reinterpret_cast<const void*>(update_tma_kernel<8, cc, st, 1>);
+    const void* fn = rows == 2 ? (wmax == 6 ? reinterpret_cast<const void*>(update_tma_kernel<6, 16, 3, 2>)
+                                            : reinterpret_cast<const void*>(update_tma_kernel<8, 16, 3, 2>))
+                               : (wmax == 6 ? reinterpret_cast<const void*>(update_tma_kernel<6, 16, 6, 1>)
+                                            : reinterpret_cast<const void*>(update_tma_kernel<8, 16, 6, 1>));
     set_smem(fn, smem);
     int cpi = static_cast<int>(cp), wi = static_cast<int>(w);
     void* args[] = {&mv, &mp, &n, &cpi, &wi, const_cast<double**>(&d_coef), &out, &ldo, const_cast<int**>(&skip)};

@@ -881,6 +881,18 @@ void set_smem(const void* kernel, size_t bytes) {
     have = bytes;
 }
 
+// Largest Gram ring stage.  Taller tiles give longer contiguous runs per
+// column (132 rows × 8 B ≈ 1 KB at 64 slots) at the price of fewer stages;
+// measured at 4000² (Gram ms per cycle): 36 KB 9.16, 50 KB 8.94, 62 KB
+// 8.82, 70 KB 8.77, 80 KB 8.83–9.03, 101 KB 8.82.  KRY_GRAM_STAGE_KB overrides.
+size_t gram_stage_bytes() {
+    static const size_t b = [] {
+        const char* e = std::getenv("KRY_GRAM_STAGE_KB");
+        return static_cast<size_t>(e ? std::atoi(e) : 70) * 1024;
+    }();
+    return b;
+}
+
 TsParams geometry(i64 n, int w, int cp, bool gram) {
     TsParams p{};
     p.n = n;
@@ -894,7 +906,7 @@ TsParams geometry(i64 n, int w, int cp, bool gram) {
         static const int cand[] = {244, 196, 132, 68};
         p.tr = 68;
         for (int c : cand)
-            if (static_cast<size_t>(c) * slots * 8 <= 36 * 1024) {
+            if (static_cast<size_t>(c) * slots * 8 <= gram_stage_bytes()) {
                 p.tr = c;
                 break;
             }

@@ -1,29 +1,30 @@
-// Tall-skinny BlkOrtho kernels for sm_100a (K3 fused Gram, K5 fused update).
+// Tall-skinny BlkOrtho kernels for sm_100a (K3 fused Gram, K5/K5t/K5b updates).
 //
-// Both stream a row tile of [V | P] (V = the block being orthogonalized,
-// w ≤ 64 columns; P = a group of prefix basis columns) from HBM into shared
-// memory with one 2-D TMA load per operand per tile (cp.async.bulk.tensor,
-// mbarrier complete_tx), through an S-stage ring driven by one producer warp,
-// and consume it with four compute warps.  Every byte of [V | P] is read from
-// HBM once per launch.
+// The Gram and the TMA updates stream row tiles of [V | P] (V = the block
+// being orthogonalized, w ≤ 64 columns; P = prefix basis columns) from HBM
+// into shared memory with 2-D TMA loads (cp.async.bulk.tensor, mbarrier
+// complete_tx) through a multi-stage ring driven by one producer warp, and
+// consume them with 4–8 compute warps.  Every byte is read from HBM once per
+// launch.
 //
-//  * gram_kernel<NBW>: G = [V | P]ᵀ·V on the DMMA pipe (mma.m8n8k4 f64).
-//    The Gram is the reduction over rows, so rows are the MMA k dimension and
-//    an 8×8 output tile is spread over the 32 lanes (2 doubles per lane): the
-//    whole (c0+w)×w output (≤ 36 tiles, upper triangle only for VᵀV, which
-//    is what gram() computes, dense_kernels.hpp:95-105) stays in registers
-//    for the whole launch.  A fragment for column block b is the same for
-//    the A and the B operand, so one conflict-free LDS per block per four
-//    rows feeds every tile of that block.  Per-CTA partials are reduced by
+//  * gram_kernel<NBW, NB, NX>: G = [V | P]ᵀ·V on the DMMA pipe (mma.m8n8k4
+//    f64).  The Gram is the reduction over rows, so rows are the MMA k
+//    dimension and an 8×8 output tile is spread over the 32 lanes (2 doubles
+//    per lane): the whole (c0+w)×w output (≤ 36 tiles, upper triangle only
+//    for VᵀV, which is what gram() computes, dense_kernels.hpp:95-105) stays
+//    in registers for the launch.  A fragment for column block b is the same
+//    for the A and the B operand, so one conflict-free LDS per block per four
+//    rows feeds every tile of that block.  NX extra tiles return panel-Gram
+//    pieces (kb_store.cpp).  Per-CTA partials are reduced by
 //    gram_reduce_kernel in a fixed order (deterministic, no float atomics).
-//  * update_kernel<WMAX>: Q = (V − P·R_col)·R_jj⁻¹ row-locally (direct coalesced
-//    streaming, see below), the order of
-//    bcgs_pip_partial's update + tri_solve_right (block_ortho.hpp:171-176,
-//    dense_kernels.hpp:139-154): vhat_j = V_j − Σ_l R_col(l,j)·p_l (l
-//    ascending), x_j = vhat_j − Σ_{l<j} R(l,j)·x_l, x_j *= 1/R(j,j).  Two
-//    adjacent rows per thread (16-byte loads), coefficients broadcast from
-//    shared memory, output written coalesced (may alias V: in place over the
-//    basis store).
+//  * update_tma_kernel (K5t) / update_kernel (K5): Q = (V − P·R_col)·R_jj⁻¹
+//    row-locally in the order of bcgs_pip_partial's update + tri_solve_right
+//    (block_ortho.hpp:171-176, dense_kernels.hpp:139-154): vhat_j = V_j −
+//    Σ_l R_col(l,j)·p_l (l ascending), x_j = vhat_j − Σ_{l<j} R(l,j)·x_l,
+//    x_j *= 1/R(j,j).  K5t streams P through a TMA ring in 16-column chunks,
+//    K5 loads it directly; both write the block in place over the store.
+//  * update_pair_kernel (w 33..64) and update_mma_kernel (K5b, a DMMA GEMM
+//    against the explicit inverse for well-conditioned wide R).
 #include <cuda.h>
 #include <cuda_runtime.h>
 #include <cudaTypedefs.h>
@@ -96,8 +97,6 @@ struct TsParams {
     int vv;         // gram: compute the VᵀV tiles in this pass
     int consumers;  // consumer warps (empty-barrier arrival count)
     int xb0;        // gram: first extra P slot block (NX > 0)
-    int first;      // update: V holds the raw block (else the running partial)
-    int last;       // update: apply the triangular solve and the scaling
     unsigned tx_bytes;
 };
 

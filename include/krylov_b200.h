@@ -31,7 +31,7 @@
 extern "C" {
 #endif
 
-#define KRY_ABI_VERSION 1
+#define KRY_ABI_VERSION 2
 
 /* ---- status codes (reference exceptions, types.hpp) -------------------- */
 enum kry_status {
@@ -129,6 +129,9 @@ typedef struct kry_report {
     int64_t update_launches;
     int64_t gpu_launches;          /* every kernel this library launched */
     int64_t allreduces;            /* device collectives issued (Gram + norms) */
+    double fused_kernel_seconds;   /* fused first-stage pass (update → MPK → Gram), k_fused.cu */
+    double fused_bytes;            /* its necessary HBM bytes: prefix + raw block read, 2 blocks written */
+    int64_t fused_launches;
 } kry_report;
 
 /* ---- library ------------------------------------------------------------ */

@@ -223,7 +223,8 @@ def _report_from_c(rep: kry_report, cyc, pb, pbp, solution) -> SolveReport:
     tel = {k: getattr(rep, k) for k in (
         "mpk_seconds", "ortho_seconds", "gram_kernel_seconds", "update_kernel_seconds",
         "restart_seconds", "mpk_bytes", "ortho_bytes", "gram_bytes", "update_bytes",
-        "gram_launches", "update_launches", "gpu_launches", "allreduces")}
+        "gram_launches", "update_launches", "gpu_launches", "allreduces",
+        "fused_kernel_seconds", "fused_bytes", "fused_launches")}
     return SolveReport(
         status=SolveStatus(rep.status), iterations=rep.iterations, restarts=rep.restarts,
         initial_residual=rep.initial_residual, final_relative_residual=rep.final_relative_residual,

@@ -55,6 +55,7 @@ class kry_report(C.Structure):
         ("update_kernel_seconds", dbl), ("restart_seconds", dbl), ("mpk_bytes", dbl),
         ("ortho_bytes", dbl), ("gram_bytes", dbl), ("update_bytes", dbl),
         ("gram_launches", i64), ("update_launches", i64), ("gpu_launches", i64), ("allreduces", i64),
+        ("fused_kernel_seconds", dbl), ("fused_bytes", dbl), ("fused_launches", i64),
     ]
 
 

@@ -1,0 +1,493 @@
+// K6: the fused first-stage pass of the speculative two-stage path, 2-D
+// 5-point stencil, one rank.
+//
+// Between two first-stage blocks the unfused path streams the basis prefix
+// Q[:, 0:c0] twice: once in block j's update (K5t: Q_j = (V_j − P·R_col)·R_jj⁻¹)
+// and again in block j+1's Gram (K3: [Q[:, 0:c0'] | V_{j+1}]ᵀ·V_{j+1}), with
+// block j+1's MPK (K2f) in between, because V_{j+1} = A^k·q (q = Q_j's last
+// column) needs the updated block.  For a stencil every row of V_{j+1} only
+// depends on rows of q within s grid lines / columns, so the three steps can
+// run in one pass over the rows: K6 updates a window of rows of block j,
+// feeds the new q into the s-level stencil wavefront and, s lines later,
+// accumulates the Gram of block j+1 over the same rows while they are still
+// in L2.  The prefix then crosses HBM once per block instead of twice.
+//
+// Work decomposition.  The grid is cut into 64-column windows (32 lanes ×
+// double2) that output their middle 64 − 2H columns (H = S rounded up to
+// even, as K2f), and the window-major (window, line) index space is split
+// into one contiguous range per CTA (1–3 window segments each).  A segment
+// [y0, y1) of window wx runs y1 − y0 + 2S line steps: the update computes
+// lines y0 − S … y1 + S − 1 (the 2S lines outside the segment and the H
+// halo columns are recomputed for the wavefront, never stored), level k of
+// the MPK trails the update by k lines, and the Gram takes line y0 + g at
+// step g + 2S.  Roles inside a CTA, synchronised by mbarrier rings:
+//   * kFuU update warps, one line per step round robin: update_acc (K5's
+//     arithmetic, term for term → bit-identical to K5/K5t), stores block j
+//     in place (core rows of the segment only), q into the next raw block,
+//     and q of all 64 columns into a shared ring for the MPK warp;
+//   * one MPK warp: the S-level skewed wavefront of K2f (same element order
+//     → bit-identical to S spmv calls), storing levels 1..S of the next raw
+//     block; signals the Gram when level S of a line is stored;
+//   * kFuG Gram warps, one line per step round robin: K3's DMMA tiles with
+//     rows as the MMA k dimension, fragments loaded from L2 (the rows were
+//     streamed or written ≤ 2S steps earlier), plus the panel-Gram pieces
+//     (NX extra tiles, kb_store.cpp).  Per-CTA partials in K3's packed tile
+//     layout, reduced by gram_reduce_kernel in a fixed order.
+//
+// Races.  Windows overlap by 2H columns and segments recompute 2S lines, so
+// a CTA reads rows another CTA owns.  Both raw blocks therefore live outside
+// the store (Store::fraw_, double-buffered): the update reads raw block j
+// there and writes the store; the MPK writes raw block j+1 to the other
+// buffer.  The prefix Q[:, 0:c0] is read-only in the pass.
+#include <cuda.h>
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstdlib>
+#include <type_traits>
+
+#include "kb_common.hpp"
+#include "kb_device.hpp"
+#include "kb_kernels.hpp"
+
+namespace kb {
+
+namespace {
+
+using namespace dev;
+
+constexpr int kFuU = 2;   // update warps
+constexpr int kFuG = 6;   // Gram warps
+constexpr int kFuMpk = kFuU, kFuProd = kFuU + 1, kFuG0 = kFuU + 2;
+constexpr int kFuWarps = kFuG0 + kFuG;
+constexpr int kFuThreads = kFuWarps * 32;
+constexpr int kQR = 2;    // q ring (update → MPK), lines; a multiple of kFuU
+constexpr int kGR = 6;    // Gram ring (MPK → Gram), lines; a multiple of kFuG
+constexpr int kBox = 68;  // rows per slot column: the 64-row window + 4 (≡ 4 mod 16: conflict-free DMMA fragments)
+constexpr int kMaxSlots = 12;
+
+struct FusedMaps {
+    CUtensorMap p;  // store columns [0, c0): box kBox × c0
+    CUtensorMap v;  // raw block j: box kBox × w
+};
+
+// One slot holds window line l: [prefix Q[:, 0:c0] | raw block j] (kBox rows
+// each).  The update overwrites the raw block with Q_j in place, and the slot
+// stays until the Gram of line l (S lines later) has read [prefix | Q_j] —
+// so the prefix crosses HBM once and is never re-read.  Slots live for
+// S + 2 lines; a line's full/empty barriers are indexed by line mod 2·nslots
+// so every parity wait is at most one phase ahead.
+//
+// Tile order of gram_kernel<1, NB, NX>: (jb = 0, ib = 0..NB−1), then the
+// extra tiles (k, ib = 1..NB−1).
+template <int S, int WMAX, int NB, int NX>
+__global__ void __launch_bounds__(kFuThreads, 1)
+    fused_pass_kernel(const __grid_constant__ FusedMaps maps, const FusedPassArgs a, int nslots) {
+    if (a.skip && *a.skip) return;  // block j's factorisation failed: nothing may change (k_pip.cu)
+    constexpr int H = (S + 1) & ~1, STEP = 64 - 2 * H;
+    static_assert(STEP % 4 == 0, "core columns must split into 4-row DMMA chunks");
+    static_assert(WMAX == S + 1, "the raw block is the MPK block");
+    constexpr int T = NB + NX * (NB - 1);
+    extern __shared__ __align__(1024) unsigned char smem[];
+    const int cp = a.c0;
+    // TMA destinations must be 128-byte aligned: the raw block starts at voff
+    const int voff = (cp * kBox + 15) / 16 * 16;
+    const int slot_doubles = voff + (WMAX * kBox + 15) / 16 * 16;
+    double* ring = reinterpret_cast<double*>(smem);  // [nslots][cp + w][kBox]; Gram scratch at the end
+    const size_t ring_doubles = max(static_cast<size_t>(nslots) * slot_doubles, static_cast<size_t>(kFuG) * T * 64);
+    const int nbar = 2 * nslots;
+    uint64_t* lfull = reinterpret_cast<uint64_t*>(ring + ring_doubles);  // [2·kMaxSlots]
+    uint64_t* lfree = lfull + 2 * kMaxSlots;                             // [2·kMaxSlots]
+    uint64_t* qfull = lfree + 2 * kMaxSlots;
+    uint64_t* qempty = qfull + kQR;
+    uint64_t* gready = qempty + kQR;
+    uint64_t* gempty = gready + kGR;
+    double2* qring = reinterpret_cast<double2*>(gempty + kGR);  // [kQR][32]
+    double* c_sm = reinterpret_cast<double*>(qring + kQR * 32);  // −R_col [cp][WMAX], −R_jj, 1/r_jj
+    for (int i = threadIdx.x; i < (cp + WMAX + 1) * WMAX; i += blockDim.x) c_sm[i] = a.coef[i];
+    if (threadIdx.x == 0) {
+        for (int i = 0; i < 2 * kMaxSlots; ++i) {
+            mbar_init(&lfull[i], 1);
+            mbar_init(&lfree[i], 1);
+        }
+        for (int i = 0; i < kQR; ++i) {
+            mbar_init(&qfull[i], 1);
+            mbar_init(&qempty[i], 1);
+        }
+        for (int i = 0; i < kGR; ++i) {
+            mbar_init(&gready[i], 1);
+            mbar_init(&gempty[i], 1);
+        }
+        asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+    }
+    __syncthreads();
+
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    const int nx = a.nx, ny = a.ny;
+    const i64 ld = a.ld, nx64 = nx;
+    // Tasks (window wx, band b) in window-major order, task i on CTA i mod
+    // grid: the CTAs of one round cover whole runs of windows at the same
+    // band, so neighbouring windows pass the same lines at the same time (the
+    // overlapping halo columns hit L2), and bands alternate direction so the
+    // 2S lines recomputed at a band seam are the ones the neighbouring band
+    // processes at the same moment (both reach the seam at the end).
+    auto for_tasks = [&](auto&& body) {
+        for (int task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
+            const int wx = task / a.nbands, b = task % a.nbands;
+            const int y0 = static_cast<int>(static_cast<i64>(b) * ny / a.nbands);
+            const int y1 = static_cast<int>(static_cast<i64>(b + 1) * ny / a.nbands);
+            body(wx, y0, y1, (b & 1) != 0);
+        }
+    };
+    // line of update step t; levels trail the update by k lines, the Gram by S
+    auto step_line = [&](int y0, int y1, bool down, int t) { return down ? y1 - 1 + S - t : y0 - S + t; };
+    // Steps t < S and t ≥ len + S are recomputed lines outside the band: no
+    // Gram, the update frees their slot.  In-band line of step t: Gram g = t − S.
+    auto slot_of = [&](int tt) { return ring + static_cast<size_t>(tt % nslots) * slot_doubles; };
+
+    if (warp == kFuProd) {
+        // ---- TMA producer: window line of [prefix | raw block j] per slot ---
+        if (lane != 0) return;
+        const unsigned tx = static_cast<unsigned>(cp + WMAX) * kBox * 8;
+        int ub = 0;
+        for_tasks([&](int wx, int y0, int y1, bool down) {
+            const int steps = y1 - y0 + 2 * S;
+            const int ix0 = wx * STEP - H;
+            for (int t = 0; t < steps; ++t) {
+                const int ut = ub + t;
+                if (ut >= nslots) {
+                    const int pt = ut - nslots;  // the line this slot held
+                    mbar_wait(&lfree[pt % nbar], (pt / nbar) & 1);
+                }
+                // rows outside [0, n) (lines off the grid) are zero-filled by TMA
+                const int row0 = step_line(y0, y1, down, t) * nx + ix0;
+                double* st = slot_of(ut);
+                uint64_t* bar = &lfull[ut % nbar];
+                mbar_expect_tx(bar, tx);
+                if (cp > 0) tma_load_2d(st, &maps.p, row0, 0, bar);
+                tma_load_2d(st + voff, &maps.v, row0, 0, bar);
+            }
+            ub += steps;
+        });
+    } else if (warp < kFuU) {
+        // ---- update of block j from the slot (K5's arithmetic, term for term)
+        const double* nrc = c_sm;
+        const double* nrjj = c_sm + cp * WMAX;
+        const double* inv = nrjj + WMAX * WMAX;
+        double* outj = a.Q + cp * ld;  // store columns [cp, cp + w)
+        int tb = 0;
+        for_tasks([&](int wx, int y0, int y1, bool down) {
+            const int ix = wx * STEP - H + 2 * lane;
+            const bool in_grid = ix >= 0 && ix < nx;
+            const bool store_lane = in_grid && lane >= H / 2 && lane < 32 - H / 2;
+            const int steps = y1 - y0 + 2 * S;
+            for (int t = ((warp - tb) % kFuU + kFuU) % kFuU; t < steps; t += kFuU) {  // tt ≡ warp (mod kFuU)
+                const int tt = tb + t;
+                mbar_wait(&lfull[tt % nbar], (tt / nbar) & 1);
+                double* st = slot_of(tt) + 2 * lane;
+                double acc[WMAX][2];
+#pragma unroll
+                for (int j = 0; j < WMAX; ++j) {
+                    const double2 v = *reinterpret_cast<const double2*>(st + voff + j * kBox);
+                    acc[j][0] = v.x;
+                    acc[j][1] = v.y;
+                }
+#pragma unroll 4
+                for (int l = 0; l < cp; ++l) {
+                    const double2 pv = *reinterpret_cast<const double2*>(st + l * kBox);
+                    const double2* cr = reinterpret_cast<const double2*>(nrc + l * WMAX);
+#pragma unroll
+                    for (int j = 0; j < WMAX; j += 2) {
+                        const double2 c = cr[j / 2];
+                        acc[j][0] = fma(c.x, pv.x, acc[j][0]);
+                        acc[j][1] = fma(c.x, pv.y, acc[j][1]);
+                        acc[j + 1][0] = fma(c.y, pv.x, acc[j + 1][0]);
+                        acc[j + 1][1] = fma(c.y, pv.y, acc[j + 1][1]);
+                    }
+                }
+                update_tri<WMAX, 2>(acc, nrjj, inv);
+                const int l = step_line(y0, y1, down, t);
+                const bool live = in_grid && l >= 0 && l < ny;
+                const bool in_band = t >= S && t < steps - S;
+                const double2 q = live ? make_double2(acc[WMAX - 1][0], acc[WMAX - 1][1]) : make_double2(0.0, 0.0);
+                if (in_band) {
+                    // Q_j over the raw block in the slot, for this line's Gram
+#pragma unroll
+                    for (int j = 0; j < WMAX; ++j)
+                        *reinterpret_cast<double2*>(st + voff + j * kBox) = make_double2(acc[j][0], acc[j][1]);
+                    if (live && store_lane) {
+                        const i64 row = static_cast<i64>(l) * nx64 + ix;
+#pragma unroll
+                        for (int j = 0; j < WMAX; ++j) RowVec<2>::st(outj + row + j * ld, acc[j]);  // w == WMAX
+                        *reinterpret_cast<double2*>(a.Vn + row) = q;  // seam: column 0 of raw block j+1
+                    }
+                    // the slot is refilled by TMA (async proxy) once the Gram frees it
+                    asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+                }
+                const int qs = tt % kQR;
+                if (tt >= kQR) mbar_wait(&qempty[qs], ((tt / kQR) - 1) & 1);
+                qring[qs * 32 + lane] = q;
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&qfull[qs]);
+                    if (!in_band) mbar_arrive(&lfree[tt % nbar]);  // recomputed line: no Gram
+                }
+            }
+            tb += steps;
+        });
+    } else if (warp == kFuMpk) {
+        // ---- MPK of block j+1: levels 1..S of the q wavefront ---------------
+        // A[k], B[k], C[k]: level k at lines l − k, l − k − 1, l − k − 2 after step l.
+        int tb = 0, gb = 0;
+        for_tasks([&](int wx, int y0, int y1, bool down) {
+            const int ix = wx * STEP - H + 2 * lane;
+            const bool in_grid = ix >= 0 && ix < nx;
+            const bool store_lane = in_grid && lane >= H / 2 && lane < 32 - H / 2;
+            double2 A[S + 1], B[S + 1], C[S + 1];
+#pragma unroll
+            for (int k = 0; k <= S; ++k) A[k] = B[k] = C[k] = make_double2(0.0, 0.0);
+            const int steps = y1 - y0 + 2 * S;
+            for (int t = 0; t < steps; ++t) {
+                const int tt = tb + t, slot = tt % kQR;
+                mbar_wait(&qfull[slot], (tt / kQR) & 1);
+                const double2 in = qring[slot * 32 + lane];
+                __syncwarp();
+                if (lane == 0) mbar_arrive(&qempty[slot]);
+                const int l = step_line(y0, y1, down, t);
+                C[0] = B[0];
+                B[0] = A[0];
+                A[0] = in;
+#pragma unroll
+                for (int k = 1; k <= S; ++k) {
+                    // ascending: A = line lk + 1, C = lk − 1; descending: the reverse
+                    const double2 dn = down ? A[k - 1] : C[k - 1], cu = B[k - 1], up = down ? C[k - 1] : A[k - 1];
+                    const double left = __shfl_up_sync(0xffffffffu, cu.y, 1);
+                    const double right = __shfl_down_sync(0xffffffffu, cu.x, 1);
+                    // spmv's stored order: row−nx, row−1, row, row+1, row+nx (K2f)
+                    double s0 = __dadd_rn(0.0, -dn.x);
+                    s0 = __dadd_rn(s0, -left);
+                    s0 = __dadd_rn(s0, __dmul_rn(4.0, cu.x));
+                    s0 = __dadd_rn(s0, -cu.y);
+                    s0 = __dadd_rn(s0, -up.x);
+                    double s1 = __dadd_rn(0.0, -dn.y);
+                    s1 = __dadd_rn(s1, -cu.x);
+                    s1 = __dadd_rn(s1, __dmul_rn(4.0, cu.y));
+                    s1 = __dadd_rn(s1, -right);
+                    s1 = __dadd_rn(s1, -up.y);
+                    const int lk = down ? l + k : l - k;
+                    const bool live = in_grid && lk >= 0 && lk < ny;
+                    const double2 v = live ? make_double2(s0, s1) : make_double2(0.0, 0.0);
+                    C[k] = B[k];
+                    B[k] = A[k];
+                    A[k] = v;
+                    if (store_lane && lk >= y0 && lk < y1)
+                        *reinterpret_cast<double2*>(a.Vn + k * ld + static_cast<i64>(lk) * nx64 + ix) = v;
+                }
+                const int g = t - 2 * S;  // the segment's g-th line (l ∓ S) is complete
+                if (g >= 0 && g < y1 - y0) {
+                    const int gg = gb + g, gs = gg % kGR;
+                    if (gg >= kGR) mbar_wait(&gempty[gs], ((gg / kGR) - 1) & 1);
+                    __syncwarp();
+                    if (lane == 0) mbar_arrive(&gready[gs]);
+                }
+            }
+            tb += steps;
+            gb += y1 - y0;
+        });
+    } else {
+        // ---- Gram of block j+1: [V_{j+1} | Q[:, 0:c0']]ᵀ·V_{j+1} --------------
+        const int gw = warp - kFuG0;
+        double acc[NB][2];
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib) acc[ib][0] = acc[ib][1] = 0.0;
+        double accx[NX > 0 ? NX : 1][NB][2];
+#pragma unroll
+        for (int k = 0; k < (NX > 0 ? NX : 1); ++k)
+#pragma unroll
+            for (int ib = 0; ib < NB; ++ib) accx[k][ib][0] = accx[k][ib][1] = 0.0;
+        const int m = lane >> 2, kq = lane & 3;
+        // slot block 0 = [q | levels 1..S | 0 0]: q (Q_j's last column) from the
+        // slot, the levels from the next raw block (global, written ≤ 2 lines
+        // ago by the MPK warp); blocks b ≥ 1 = prefix columns 8(b−1) + m of
+        // [Q[:, 0:c0] | Q_j] < c0n, all from the slot
+        const int c0n = a.c0n;
+        const double* lev = a.Vn + m * ld;
+        const bool lev_on = m >= 1 && m < a.w;
+        int gb = 0, tb = 0;
+        for_tasks([&](int wx, int y0, int y1, bool down) {
+            const int len = y1 - y0;
+            for (int g = ((gw - gb) % kFuG + kFuG) % kFuG; g < len; g += kFuG) {  // gg ≡ gw (mod kFuG)
+                const int gg = gb + g, gs = gg % kGR;
+                mbar_wait(&gready[gs], (gg / kGR) & 1);
+                const int line = down ? y1 - 1 - g : y0 + g;
+                const int tt = tb + g + S;  // update step of this line
+                const double* st = slot_of(tt) + H + kq;  // core rows start at slot row H
+                const int cbase = wx * STEP + kq;
+                const i64 rbase = static_cast<i64>(line) * nx64 + cbase;
+                // the line's level fragments (global) in one batch: one L2 round trip per line
+                double lv[STEP / 4];
+#pragma unroll
+                for (int c = 0; c < STEP / 4; ++c)
+                    lv[c] = (lev_on && cbase + 4 * c < nx) ? lev[rbase + 4 * c] : 0.0;
+#pragma unroll
+                for (int c = 0; c < STEP / 4; ++c) {
+                    const bool ok = cbase + 4 * c < nx;
+                    double f[NB];
+                    f[0] = !ok ? 0.0 : m == 0 ? st[voff + (WMAX - 1) * kBox + 4 * c] : lv[c];
+#pragma unroll
+                    for (int b = 1; b < NB; ++b) {
+                        const int col = 8 * (b - 1) + m;
+                        f[b] = (ok && col < c0n) ? st[(col < cp ? col * kBox : voff + (col - cp) * kBox) + 4 * c] : 0.0;
+                    }
+#pragma unroll
+                    for (int ib = 0; ib < NB; ++ib) dmma(acc[ib][0], acc[ib][1], f[ib], f[0]);
+                    if constexpr (NX > 0) {
+#pragma unroll
+                        for (int k = 0; k < NX; ++k) {
+                            const int xb = a.xb0 + k;
+                            double fx = 0.0;
+#pragma unroll
+                            for (int b = 1; b < NB; ++b)
+                                if (b == xb) fx = f[b];
+#pragma unroll
+                            for (int ib = 1; ib < NB; ++ib)
+                                if (ib <= xb) dmma(accx[k][ib][0], accx[k][ib][1], f[ib], fx);
+                        }
+                    }
+                }
+                __syncwarp();
+                if (lane == 0) {
+                    mbar_arrive(&gempty[gs]);
+                    mbar_arrive(&lfree[tt % nbar]);
+                }
+            }
+            gb += len;
+            tb += len + 2 * S;
+        });
+        // cross-warp sums in fixed warp order (K3's packed tile layout), through
+        // the update ring: idle once the last Gram line is ready
+        asm volatile("bar.sync 1, %0;" ::"n"(kFuG * 32));
+        double* scratch = ring;
+        const int e0 = (lane >> 2) + 8 * (2 * (lane & 3));
+#pragma unroll
+        for (int ib = 0; ib < NB; ++ib) {
+            double* t = scratch + (static_cast<size_t>(gw) * T + ib) * 64;
+            t[e0] = acc[ib][0];
+            t[e0 + 8] = acc[ib][1];
+        }
+        if constexpr (NX > 0) {
+#pragma unroll
+            for (int k = 0; k < NX; ++k)
+#pragma unroll
+                for (int ib = 1; ib < NB; ++ib) {
+                    double* t = scratch + (static_cast<size_t>(gw) * T + NB + k * (NB - 1) + (ib - 1)) * 64;
+                    t[e0] = accx[k][ib][0];
+                    t[e0 + 8] = accx[k][ib][1];
+                }
+        }
+        asm volatile("bar.sync 1, %0;" ::"n"(kFuG * 32));
+        constexpr int per_cta = T * 64;
+        double* out = a.partials + static_cast<size_t>(blockIdx.x) * per_cta;
+        for (int e = gw * 32 + lane; e < per_cta; e += kFuG * 32) {
+            double sum = scratch[e];
+#pragma unroll
+            for (int v = 1; v < kFuG; ++v) sum += scratch[static_cast<size_t>(v) * per_cta + e];
+            out[e] = sum;
+        }
+    }
+}
+
+template <int S, int WMAX, int NB>
+const void* fused_fn_nb(int nb, int nx) {
+    if (nb == NB) {
+        if (nx == 0) return reinterpret_cast<const void*>(fused_pass_kernel<S, WMAX, NB, 0>);
+        if constexpr (NB > 1) {
+            if (nx == 1) return reinterpret_cast<const void*>(fused_pass_kernel<S, WMAX, NB, 1>);
+            if (nx == 2) return reinterpret_cast<const void*>(fused_pass_kernel<S, WMAX, NB, 2>);
+        }
+        return nullptr;
+    }
+    if constexpr (NB < 8) return fused_fn_nb<S, WMAX, NB + 1>(nb, nx);
+    return nullptr;
+}
+
+constexpr size_t kFuSmem = 225 * 1024;
+size_t fused_slot_bytes(i64 c0) { return static_cast<size_t>(round_up(c0 * kBox, 16) + round_up(6 * kBox, 16)) * 8; }
+size_t fused_fixed_smem(i64 c0) {
+    return static_cast<size_t>(4 * kMaxSlots + 2 * kQR + 2 * kGR) * 8 + static_cast<size_t>(kQR) * 32 * 16 +
+           static_cast<size_t>(c0 + 7) * 6 * 8;
+}
+
+}  // namespace
+
+bool fused_pass_supported(const StencilGeom& g, int s, i64 w, i64 c0n, i64 ld, const double* Q,
+                          const double* V, const double* Vn) {
+    auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    return g.dims == 2 && g.line0 == 0 && g.lines == g.ny && (g.nx & 1) == 0 && s == 5 && w == s + 1 &&
+           update_wmax(w) == 6 && c0n + w <= 64 && (ld & 1) == 0 && a16(Q) && a16(V) && a16(Vn) &&
+           // the widest fused update (prefix c0n − w + 1) still gets S + 2 ring slots
+           static_cast<size_t>(s + 2) * fused_slot_bytes(c0n - w + 1) + fused_fixed_smem(c0n - w + 1) <= kFuSmem &&
+           g.nx + 64 < (i64(1) << 31) && g.ny < (i64(1) << 30);
+}
+
+i64 fused_partials_doubles() { return static_cast<i64>(device_sms()) * (8 + 2 * 7) * 64; }
+
+void launch_fused_pass(cudaStream_t stream, const StencilGeom& g, int s, FusedPassArgs a, double* d_packed,
+                       int64_t& launches) {
+    const int h = (s + 1) & ~1, step = 64 - 2 * h;
+    const int nb = 1 + static_cast<int>(round_up(a.c0n, 8) / 8);
+    int nxt = 0;
+    if (a.x_count > 0) {
+        const int s0 = 8 + a.x_first, s1 = s0 + a.x_count - 1;
+        a.xb0 = s0 / 8;
+        nxt = s1 / 8 - a.xb0 + 1;
+        if (nxt > 2 || s1 / 8 >= nb) fail(KRY_INTERNAL, "fused pass: extra-column shape");
+    } else {
+        a.xb0 = 0;
+    }
+    const void* fn = s == 5 ? fused_fn_nb<5, 6, 1>(nb, nxt) : nullptr;
+    if (!fn) fail(KRY_UNSUPPORTED, "fused pass shape");
+    a.nx = static_cast<int>(g.nx);
+    a.ny = static_cast<int>(g.ny);
+    const i64 nwx = ceil_div(g.nx, step);
+    const i64 sms = device_sms();
+    // bands per window: minimise rounds × (band + 2S) line steps per CTA
+    {
+        i64 best = -1, best_cost = 0;
+        for (i64 nb = 1; nb <= std::max<i64>(1, g.ny / (4 * s)) && nb <= 4096; ++nb) {
+            const i64 tasks = nwx * nb, rounds = ceil_div(tasks, sms);
+            const i64 cost = rounds * (ceil_div(g.ny, nb) + 2 * s);
+            if (best < 0 || cost < best_cost) {
+                best = nb;
+                best_cost = cost;
+            }
+        }
+        a.nbands = static_cast<int>(best);
+        a.ntasks = static_cast<int>(nwx * best);
+    }
+    const int T = nb + nxt * (nb - 1);
+    FusedMaps maps{};
+    // window lines start at arbitrary rows: no 256-byte L2 promotion (it would
+    // fetch three 256-byte sectors groups per 512-byte column run)
+    if (a.c0 > 0) maps.p = dev::tensor_map_2d(a.Q, a.ld, g.nloc, a.c0, kBox, a.c0, false);
+    maps.v = dev::tensor_map_2d(a.V, a.ld, g.nloc, a.w, kBox, a.w, false);
+    // ring slots: a line's slot lives from its TMA load until its Gram, S
+    // lines after its update, so at least S + 2 (one line of prefetch)
+    const size_t slot_bytes = fused_slot_bytes(a.c0);
+    const size_t fixed = fused_fixed_smem(a.c0);
+    int nslots = static_cast<int>(std::min<size_t>(kMaxSlots, (kFuSmem - fixed) / slot_bytes));
+    if (nslots < s + 2) fail(KRY_UNSUPPORTED, "fused pass: shared memory");
+    const size_t ring = std::max(static_cast<size_t>(nslots) * slot_bytes, static_cast<size_t>(kFuG) * T * 64 * 8);
+    const size_t smem = ring + fixed;
+    set_kernel_smem(fn, smem);
+    const int grid = static_cast<int>(std::max<i64>(1, std::min<i64>(sms, a.ntasks)));
+    if (static_cast<i64>(grid) * T * 64 > fused_partials_doubles()) fail(KRY_INTERNAL, "fused pass partials");
+    void* args[] = {&maps, &a, &nslots};
+    KB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kFuThreads), args, smem, stream));
+    KB_LAUNCHED();
+    launch_gram_reduce(stream, a.partials, grid, T * 64, d_packed);
+    launches += 2;
+}
+
+}  // namespace kb

@@ -37,53 +37,19 @@
 #include <vector>
 
 #include "kb_common.hpp"
+#include "kb_device.hpp"
 #include "kb_kernels.hpp"
 
 namespace kb {
 
 namespace {
 
+using namespace dev;
+
 // Consumer warps per CTA: 8 while the accumulators are small, 4 for the
 // widest Gram shapes (≥ 30 register-resident tiles) to stay spill-free.
 __host__ __device__ constexpr int consumer_warps(int nbw) { return nbw >= 5 ? 4 : 8; }
 constexpr int kSmemBudget = 200 * 1024;
-
-__device__ __forceinline__ unsigned smem_u32(const void* p) {
-    return static_cast<unsigned>(__cvta_generic_to_shared(p));
-}
-__device__ __forceinline__ void mbar_init(uint64_t* bar, unsigned count) {
-    asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
-}
-__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, unsigned bytes) {
-    asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)),
-                 "r"(bytes)
-                 : "memory");
-}
-__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
-    asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
-}
-__device__ __forceinline__ void mbar_wait(uint64_t* bar, unsigned parity) {
-    asm volatile(
-        "{\n\t.reg .pred p;\n"
-        "KB_WAIT_%=:\n\t"
-        "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
-        "@!p bra KB_WAIT_%=;\n}" ::"r"(smem_u32(bar)),
-        "r"(parity)
-        : "memory");
-}
-__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int x, int y,
-                                            uint64_t* bar) {
-    asm volatile(
-        "cp.async.bulk.tensor.2d.shared::cluster.global.tile.mbarrier::complete_tx::bytes"
-        " [%0], [%1, {%2, %3}], [%4];" ::"r"(smem_u32(dst)),
-        "l"(reinterpret_cast<uint64_t>(map)), "r"(x), "r"(y), "r"(smem_u32(bar))
-        : "memory");
-}
-__device__ __forceinline__ void dmma(double& d0, double& d1, double a, double b) {
-    asm volatile("mma.sync.aligned.m8n8k4.row.col.f64.f64.f64.f64 {%0,%1}, {%2}, {%3}, {%0,%1};"
-                 : "+d"(d0), "+d"(d1)
-                 : "d"(a), "d"(b));
-}
 
 struct TsParams {
     i64 n;          // rows
@@ -336,126 +302,6 @@ const void* gram_x_fn(int nb, int nx) {
 // coef layout (doubles): nrc[cp][WMAX] = −R_col, nrjj[WMAX][WMAX] = −R_jj(l,j)
 // for l < j, inv[WMAX] = 1/R_jj(j,j).
 // ---------------------------------------------------------------------------
-// R rows per thread (R = 2: 16-byte loads/stores of two adjacent rows —
-// half the load instructions and coefficient broadcasts per element).
-template <int R>
-struct RowVec;
-template <>
-struct RowVec<1> {
-    static __device__ __forceinline__ void ld(const double* p, double (&d)[1]) { d[0] = __ldg(p); }
-    static __device__ __forceinline__ void ldv(const double* p, double (&d)[1]) { d[0] = *p; }
-    static __device__ __forceinline__ void st(double* p, const double (&d)[1]) { *p = d[0]; }
-};
-template <>
-struct RowVec<2> {
-    static __device__ __forceinline__ void ld(const double* p, double (&d)[2]) {
-        const double2 t = __ldg(reinterpret_cast<const double2*>(p));
-        d[0] = t.x;
-        d[1] = t.y;
-    }
-    static __device__ __forceinline__ void ldv(const double* p, double (&d)[2]) {
-        const double2 t = *reinterpret_cast<const double2*>(p);
-        d[0] = t.x;
-        d[1] = t.y;
-    }
-    static __device__ __forceinline__ void st(double* p, const double (&d)[2]) {
-        *reinterpret_cast<double2*>(p) = make_double2(d[0], d[1]);
-    }
-};
-
-// Rows [row, row + R) of the update (every row computed in exactly the
-// scalar order, so R = 1 and R = 2 give identical bits).
-template <int WMAX, int R>
-__device__ __forceinline__ void update_rows(i64 row, const double* __restrict__ P, i64 ldp, int cp, int cpp,
-                                            const double* V, i64 ldv, int w, const double* nrc,
-                                            const double* nrjj, const double* inv, int triangular, double* out,
-                                            i64 ldo) {
-    using RV = RowVec<R>;
-    double acc[WMAX][R];
-#pragma unroll
-    for (int j = 0; j < WMAX; ++j) {
-        if (j < w) {
-            RV::ldv(V + row + j * ldv, acc[j]);
-        } else {
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[j][r] = 0.0;
-        }
-    }
-    // Prefix columns in batches of 4 through a 3-deep register ring: two
-    // batches are in flight while one is consumed.  The coefficient rows are
-    // zero-padded to a multiple of 12 (see the shared-memory fill), so there
-    // is no tail loop; loads past cp are predicated off.
-    const double* prow = P + row;
-    const int nb = cpp / 4;
-    double b0[4][R], b1[4][R], b2[4][R];
-    auto ld = [&](double (&dst)[4][R], int bt) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const int l = 4 * bt + u;
-            if (l < cp) {
-                RV::ld(prow + static_cast<i64>(l) * ldp, dst[u]);
-            } else {
-#pragma unroll
-                for (int r = 0; r < R; ++r) dst[u][r] = 0.0;
-            }
-        }
-    };
-    auto fm = [&](const double (&src)[4][R], int bt) {
-#pragma unroll
-        for (int u = 0; u < 4; ++u) {
-            const double2* cr = reinterpret_cast<const double2*>(nrc + (4 * bt + u) * WMAX);
-#pragma unroll
-            for (int j = 0; j < WMAX; j += 2) {
-                const double2 c = cr[j / 2];
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    acc[j][r] = fma(c.x, src[u][r], acc[j][r]);
-                    acc[j + 1][r] = fma(c.y, src[u][r], acc[j + 1][r]);
-                }
-            }
-        }
-    };
-    if (nb > 0) {
-        ld(b0, 0);
-        ld(b1, 1);
-    }
-    for (int bt = 0; bt < nb; bt += 3) {  // nb is a multiple of 3
-        ld(b2, bt + 2);
-        fm(b0, bt);
-        ld(b0, bt + 3);
-        fm(b1, bt + 1);
-        ld(b1, bt + 4);
-        fm(b2, bt + 2);
-    }
-    if (triangular) {
-        // Right-looking substitution: acc_j receives −R(k,j)·x_k for
-        // k = 0, 1, … in order, then ×1/R(j,j) — tri_solve_right's order.
-#pragma unroll
-        for (int k = 0; k < WMAX; ++k) {
-#pragma unroll
-            for (int r = 0; r < R; ++r) acc[k][r] *= inv[k];
-            const double* rk = nrjj + k * WMAX;
-            if ((k + 1) & 1) {  // odd first column: one scalar step to reach a pair boundary
-                if (k + 1 < WMAX)
-#pragma unroll
-                    for (int r = 0; r < R; ++r) acc[k + 1][r] = fma(rk[k + 1], acc[k][r], acc[k + 1][r]);
-            }
-#pragma unroll
-            for (int j = (k + 2) & ~1; j < WMAX; j += 2) {
-                const double2 c = *reinterpret_cast<const double2*>(rk + j);
-#pragma unroll
-                for (int r = 0; r < R; ++r) {
-                    acc[j][r] = fma(c.x, acc[k][r], acc[j][r]);
-                    acc[j + 1][r] = fma(c.y, acc[k][r], acc[j + 1][r]);
-                }
-            }
-        }
-    }
-#pragma unroll
-    for (int j = 0; j < WMAX; ++j)
-        if (j < w) RV::st(out + row + j * ldo, acc[j]);
-}
-
 // R = 2 requires even ld's and 16-byte aligned P/V/out (the store's layout);
 // an odd last row is finished by the scalar path.
 template <int WMAX, int R>
@@ -802,16 +648,18 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
     return fn;
 }
 
-CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols);
+CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols,
+                       bool promote = true);
 
 // Tensor maps are cached by their parameters: the solver re-launches the same
 // (store column, shape) combinations every cycle, and an encode costs more
 // host time than the launch itself.
-CUtensorMap make_map_box(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols);
+CUtensorMap make_map_box(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols,
+                         bool promote = true);
 CUtensorMap make_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows) {
     return make_map_box(base, ld, rows, cols, box_rows, 0);
 }
-CUtensorMap make_map_box(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols) {
+CUtensorMap make_map_box(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols, bool promote) {
     struct Key {
         const double* base;
         i64 ld, rows, cols;
@@ -829,17 +677,17 @@ CUtensorMap make_map_box(const double* base, i64 ld, i64 rows, i64 cols, int box
     };
     static std::mutex mu;
     static std::unordered_map<Key, CUtensorMap, Hash> cache;
-    const Key key{base, ld, rows, cols, box_rows * 1024 + box_cols};
+    const Key key{base, ld, rows, cols, (box_rows * 1024 + box_cols) * 2 + (promote ? 1 : 0)};
     std::lock_guard<std::mutex> lock(mu);
     auto it = cache.find(key);
     if (it != cache.end()) return it->second;
     if (cache.size() > 4096) cache.clear();
-    CUtensorMap m = encode_map(base, ld, rows, cols, box_rows, box_cols);
+    CUtensorMap m = encode_map(base, ld, rows, cols, box_rows, box_cols, promote);
     cache.emplace(key, m);
     return m;
 }
 
-CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols = 0) {
+CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols, bool promote) {
     CUtensorMap m;
     std::memset(&m, 0, sizeof(m));
     if (cols <= 0 || base == nullptr) return m;  // unused operand
@@ -851,7 +699,8 @@ CUtensorMap encode_map(const double* base, i64 ld, i64 rows, i64 cols, int box_r
     cuuint32_t estr[2] = {1, 1};
     CUresult r = encode_fn()(&m, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, const_cast<double*>(base), dims,
                              strides, box, estr, CU_TENSOR_MAP_INTERLEAVE_NONE,
-                             CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                             CU_TENSOR_MAP_SWIZZLE_NONE,
+                             promote ? CU_TENSOR_MAP_L2_PROMOTION_L2_256B : CU_TENSOR_MAP_L2_PROMOTION_NONE,
                              CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
     if (r != CUDA_SUCCESS) fail(KRY_CUDA_ERROR, "cuTensorMapEncodeTiled failed");
     return m;
@@ -927,6 +776,18 @@ size_t ring_bytes(const TsParams& p) {
 }
 
 }  // namespace
+
+void launch_gram_reduce(cudaStream_t stream, const double* partials, int grid, int per_cta, double* packed) {
+    gram_reduce_kernel<<<ceil_div(static_cast<i64>(per_cta) * 32, 256), 256, 0, stream>>>(partials, grid, per_cta,
+                                                                                          packed);
+    KB_LAUNCHED();
+}
+void set_kernel_smem(const void* kernel, size_t bytes) { set_smem(kernel, bytes); }
+CUtensorMap dev::tensor_map_2d(const double* base, i64 ld, i64 rows, i64 cols, int box_rows, int box_cols,
+                               bool l2_promote) {
+    return make_map_box(base, ld, rows, cols, box_rows, box_cols, l2_promote);
+}
+int device_sms() { return sm_count(); }
 
 // Column groups of the prefix so that round_up(w,8) + round_up(group,8) ≤ 64.
 std::vector<std::pair<i64, i64>> prefix_groups(i64 c0, i64 w) {

@@ -118,8 +118,8 @@ void fill_report(const kb::Report& r, kry_report* out) {
 
 struct Snapshot {
     std::array<double, kb::PH_COUNT> sec;
-    int64_t launches, allreduces, gram_launches, update_launches;
-    double gram_bytes, update_bytes;
+    int64_t launches, allreduces, gram_launches, update_launches, fused_launches;
+    double gram_bytes, update_bytes, fused_bytes;
     explicit Snapshot(const kb::Ctx& c)
         : sec(c.seconds),
           launches(c.launches),
@@ -127,7 +127,10 @@ struct Snapshot {
           gram_launches(c.gram_launches),
           update_launches(c.update_launches),
           gram_bytes(c.gram_bytes),
-          update_bytes(c.update_bytes) {}
+          update_bytes(c.update_bytes),
+          fused_bytes(c.fused_bytes) {
+        fused_launches = c.fused_launches;
+    }
 };
 
 void fill_telemetry(const kb::Ctx& c, const Snapshot& s0, kry_report* out) {
@@ -143,6 +146,9 @@ void fill_telemetry(const kb::Ctx& c, const Snapshot& s0, kry_report* out) {
     out->update_launches = c.update_launches - s0.update_launches;
     out->gram_bytes = c.gram_bytes - s0.gram_bytes;
     out->update_bytes = c.update_bytes - s0.update_bytes;
+    out->fused_kernel_seconds = c.seconds[kb::PH_FUSED] - s0.sec[kb::PH_FUSED];
+    out->fused_bytes = c.fused_bytes - s0.fused_bytes;
+    out->fused_launches = c.fused_launches - s0.fused_launches;
 }
 
 // bcgs_pip on host views; returns the PipOut and writes q.

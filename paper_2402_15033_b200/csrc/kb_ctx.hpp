@@ -63,7 +63,7 @@ struct HostBuf {
     }
 };
 
-enum Phase { PH_MPK = 0, PH_ORTHO, PH_GRAM, PH_UPDATE, PH_RESTART, PH_COUNT };
+enum Phase { PH_MPK = 0, PH_ORTHO, PH_GRAM, PH_UPDATE, PH_RESTART, PH_FUSED, PH_COUNT };
 
 struct Ctx {
     int device = 0;
@@ -76,6 +76,8 @@ struct Ctx {
     int64_t allreduces = 0;
     double gram_bytes = 0.0, update_bytes = 0.0;  // algorithmic, this rank
     int64_t gram_launches = 0, update_launches = 0;
+    double fused_bytes = 0.0;  // K6: necessary HBM bytes (k_fused.cu), this rank
+    int64_t fused_launches = 0;
 
     // scratch
     DevBuf partials;      // reduce_grid() doubles + scalars

@@ -173,11 +173,12 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         return res;
     };
 
-    static const bool speculate_default = [] {  // KRY_SPECULATE=0: every block waits for its factorisation
+    // read per solve (tests switch them between solves)
+    const bool speculate_default = [] {  // KRY_SPECULATE=0: every block waits for its factorisation
         const char* e = std::getenv("KRY_SPECULATE");
         return !(e && std::string(e) == "0");
     }();
-    static const bool defer_last = [] {
+    const bool defer_last = [] {
         const char* e = std::getenv("KRY_DEFER_FINALIZE");
         return !(e && std::string(e) == "0");
     }();
@@ -214,20 +215,35 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
                 // then one sync replays the bookkeeping.  A failed block is
                 // redone on the synchronous path below, which handles the
                 // truncation / breakdown exactly as the reference.
+                // 2-D stencil on one rank: block j's update, block j+1's MPK
+                // and Gram in one pass (K6, k_fused.cu); the MPK is then part
+                // of the BlkOrtho phase.
                 const i64 j0 = j;
                 i64 jj = j;
+                const bool fuse = store.can_fuse(op, s);
                 for (;;) {
-                    const i64 c0 = (jj == 0) ? 0 : store.spec_filled() - 1;
-                    cudaEvent_t t0 = ctx.begin_phase();
-                    rep.mpk_bytes += store.mpk(op, c0, s) ? 8.0 * op.nloc * (s + 1.0) : s * op.bytes_per_apply();
-                    ctx.end_phase(PH_MPK, t0);
-                    cudaEvent_t t1 = ctx.begin_phase();
-                    store.preprocess_speculative(s + 1, jj != 0);
-                    ctx.end_phase(PH_ORTHO, t1);
+                    if (fuse) {
+                        cudaEvent_t t1 = ctx.begin_phase();
+                        if (jj == j0)
+                            store.spec_fused_first(op, s, jj != 0);
+                        else
+                            store.spec_fused_next(op, s);
+                        ctx.end_phase(PH_ORTHO, t1);
+                        rep.mpk_bytes += 8.0 * op.nloc * (s + 1.0);
+                    } else {
+                        const i64 c0 = (jj == 0) ? 0 : store.spec_filled() - 1;
+                        cudaEvent_t t0 = ctx.begin_phase();
+                        rep.mpk_bytes += store.mpk(op, c0, s) ? 8.0 * op.nloc * (s + 1.0) : s * op.bytes_per_apply();
+                        ctx.end_phase(PH_MPK, t0);
+                        cudaEvent_t t1 = ctx.begin_phase();
+                        store.preprocess_speculative(s + 1, jj != 0);
+                        ctx.end_phase(PH_ORTHO, t1);
+                    }
                     ++jj;
                     if (store.spec_panel_full() || jj == blocks) break;
                 }
                 cudaEvent_t t1 = ctx.begin_phase();
+                store.spec_flush();
                 const i64 f = store.resolve_speculative(rep.sync);
                 ctx.end_phase(PH_ORTHO, t1);
                 rep.iterations += s * (f < 0 ? jj - j0 : f);

@@ -37,6 +37,11 @@ void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp,
                    i64 w, const double* d_coef, bool triangular, double* out, i64 ldo, int64_t& launches,
                    const int* skip = nullptr);
 
+// Fixed-order sum of per-CTA Gram partials (K3 layout) into packed tiles.
+void launch_gram_reduce(cudaStream_t stream, const double* partials, int grid, int per_cta, double* packed);
+void set_kernel_smem(const void* kernel, size_t bytes);
+int device_sms();
+
 // ---- k_pip.cu : device BCGS-PIP factorisation (speculative first stage) --
 // Result slot of one block (doubles): [kSlotStatus] 0 = committed, p > 0 =
 // Cholesky pivot p failed, −1 = an earlier block of the chain failed;
@@ -92,6 +97,31 @@ int launch_csr_sliced(cudaStream_t s, i64 nloc, int nslices, const int32_t* cons
                       const int32_t* const* col, const double* const* vals, const double* x, const double* b,
                       double* y, double* partials, double* part_sum, int64_t& launches);
 int reduce_grid();  // fixed grid of every partial-sum kernel (determinism)
+
+// ---- k_fused.cu : K6 fused first-stage pass (update j → MPK j+1 → Gram j+1)
+struct FusedPassArgs {
+    double* Q;              // store (column-major, ld)
+    i64 ld;
+    const double* V;        // raw block j (w columns, ld), read-only
+    double* Vn;             // raw block j+1 out: column 0 = q, 1..s = A^k·q
+    int c0, w;              // block j: prefix columns, width
+    const double* coef;     // K5 coefficients of block j (k_pip.cu layout, wmax 6)
+    const int* skip;        // block j's skip flag
+    int c0n;                // block j+1 prefix columns (= c0 + w − 1)
+    int x_first, x_count;   // panel-Gram pieces of block j+1 (prefix columns)
+    double* partials;       // per-CTA Gram partials (fused_partials_doubles())
+    // set by the launcher
+    int xb0 = 0, nx = 0, ny = 0;
+    int ntasks = 0, nbands = 0;  // (window, band) tasks
+};
+bool fused_pass_supported(const StencilGeom& g, int s, i64 w, i64 c0n, i64 ld, const double* Q, const double* V,
+                          const double* Vn);
+i64 fused_partials_doubles();
+// Launches K6 and the reduce of its Gram into d_packed (K3 packed tiles of
+// block j+1, the layout launch_pip_block reads).
+void launch_fused_pass(cudaStream_t stream, const StencilGeom& g, int s, FusedPassArgs a, double* d_packed,
+                       int64_t& launches);
+
 void launch_finalize_sum(cudaStream_t s, const double* partials, int count, double* out,
                          int64_t& launches);
 void launch_scale_div(cudaStream_t s, i64 n, const double* r, double gamma, double* out,

@@ -55,6 +55,7 @@ bool Store::deferred_coefficients(const std::vector<double>& y, std::vector<doub
 
 void Store::reset() {
     pending_ = false;
+    fpend_.live = false;
     spec_.clear();
     std::fill(pready_.begin(), pready_.end(), 0);
     filled_ = 0;
@@ -95,7 +96,7 @@ bool Store::spec_panel_full() const {
     return f > b && f - b >= big_panel_size_ + 1;
 }
 
-void Store::preprocess_speculative(i64 w, bool overlap) {
+Store::SpecPlan Store::spec_plan(i64 w, bool overlap) {
     const bool first = spec_.empty();
     const i64 filled = first ? filled_ : spec_filled_;
     if (overlap && filled == 0) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: basis store capacity exceeded");
@@ -111,56 +112,149 @@ void Store::preprocess_speculative(i64 w, bool overlap) {
         spec_skip_.ensure(static_cast<size_t>(maxb) * 4);
         spec_host_.ensure(static_cast<size_t>(maxb) * kSlotDoubles * 8);
     }
-    const i64 idx = static_cast<i64>(spec_.size());
+    SpecPlan p{c0, static_cast<i64>(spec_.size()), -1, 0};
     // panel-Gram pieces (same rule as run_scheme's first-stage branch): the
     // previous block is a preprocessed block of the open panel unless this
     // is the panel's first block
     const bool prev_in_panel = !first || (!records_.empty() && states_.back() == KRY_PANEL_PREPROCESSED);
-    i64 xf = -1, xc = 0;
     if (prev_in_panel) {
         const i64 xend = std::min(c0 / 8 * 8, spec_xd_ / 8 * 8 + 16);
         if (xend > spec_xd_) {
-            xf = spec_xd_;
-            xc = xend - spec_xd_;
+            p.xf = spec_xd_;
+            p.xc = xend - spec_xd_;
         }
     }
-    // Gram (+ reduce) → allreduce → device factorisation → gated update
-    std::vector<int> tiles;
     ctx_.gram_partials.ensure(static_cast<size_t>(gram_scratch_doubles(w)) * 8);
     ctx_.gram_packed.ensure(2 * 64 * 64 * 8);
+    return p;
+}
+
+// [allreduce] → device factorisation of the packed Gram in ctx_.gram_packed.
+PipBlockArgs Store::spec_factor(const SpecPlan& p, i64 w) {
+    PipBlockArgs a{};
+    a.packed = ctx_.gram_packed.p;
+    a.nb = static_cast<int>(1 + round_up(p.c0, 8) / 8);
+    a.nx = p.xc > 0 ? static_cast<int>((8 + p.xf + p.xc - 1) / 8 - (8 + p.xf) / 8 + 1) : 0;
+    a.xb0 = p.xc > 0 ? static_cast<int>((8 + p.xf) / 8) : 0;
+    a.x_first = static_cast<int>(p.xf);
+    a.x_count = static_cast<int>(p.xc);
+    a.c0 = static_cast<int>(p.c0);
+    a.w = static_cast<int>(w);
+    a.wmax = update_wmax(w);
+    a.slot = spec_slots_.p + p.idx * kSlotDoubles;
+    a.prev_slot = p.idx > 0 ? spec_slots_.p + (p.idx - 1) * kSlotDoubles : nullptr;
+    a.coef = spec_coef_.p + p.idx * 640;
+    a.skip = spec_skip_.as<int>() + p.idx;
+    ctx_.allreduce_sum(ctx_.gram_packed.p, static_cast<size_t>(a.nb + a.nx * (a.nb - 1)) * 64);
+    launch_pip_block(ctx_.stream, a, ctx_.launches);
+    return a;
+}
+
+void Store::spec_push(const SpecPlan& p, i64 w, bool overlap, const double* raw) {
+    spec_.push_back({p.c0, w, overlap, p.xf, p.xc, raw});
+    spec_filled_ = p.c0 + w;
+    spec_bps_ = std::min(spec_bps_, p.c0);
+    if (p.xc > 0) spec_xd_ = p.xf + p.xc;
+}
+
+void Store::preprocess_speculative(i64 w, bool overlap) {
+    const SpecPlan p = spec_plan(w, overlap);
+    const i64 c0 = p.c0;
+    // Gram (+ reduce) → allreduce → device factorisation → gated update
+    std::vector<int> tiles;
     cudaEvent_t t0 = ctx_.begin_phase();
     launch_gram_pass(ctx_.stream, n_, c0 > 0 ? col(0) : nullptr, ld_, c0, col(c0), ld_, w, true,
-                     ctx_.gram_partials.p, ctx_.gram_packed.p, tiles, ctx_.launches, xf, xc);
+                     ctx_.gram_partials.p, ctx_.gram_packed.p, tiles, ctx_.launches, p.xf, p.xc);
     ctx_.end_phase(PH_GRAM, t0);
     ctx_.gram_bytes += 8.0 * n_ * (c0 + w);
     ctx_.gram_launches += 1;
-    ctx_.allreduce_sum(ctx_.gram_packed.p, tiles.size() * 64);
-    const int wmax = update_wmax(w);
-    PipBlockArgs a{};
-    a.packed = ctx_.gram_packed.p;
-    a.nb = static_cast<int>(1 + round_up(c0, 8) / 8);
-    a.nx = xc > 0 ? static_cast<int>((8 + xf + xc - 1) / 8 - (8 + xf) / 8 + 1) : 0;
-    a.xb0 = xc > 0 ? static_cast<int>((8 + xf) / 8) : 0;
-    a.x_first = static_cast<int>(xf);
-    a.x_count = static_cast<int>(xc);
-    a.c0 = static_cast<int>(c0);
-    a.w = static_cast<int>(w);
-    a.wmax = wmax;
-    a.slot = spec_slots_.p + idx * kSlotDoubles;
-    a.prev_slot = idx > 0 ? spec_slots_.p + (idx - 1) * kSlotDoubles : nullptr;
-    a.coef = spec_coef_.p + idx * 640;
-    a.skip = spec_skip_.as<int>() + idx;
-    launch_pip_block(ctx_.stream, a, ctx_.launches);
+    const PipBlockArgs a = spec_factor(p, w);
     cudaEvent_t t1 = ctx_.begin_phase();
     launch_update(ctx_.stream, n_, c0 > 0 ? col(0) : nullptr, ld_, c0, col(c0), ld_, w, a.coef, true, col(c0), ld_,
                   ctx_.launches, a.skip);
     ctx_.end_phase(PH_UPDATE, t1);
     ctx_.update_bytes += 8.0 * n_ * (c0 + 2.0 * w);
     ctx_.update_launches += 1;
-    spec_.push_back({c0, w, overlap, xf, xc});
-    spec_filled_ = c0 + w;
-    spec_bps_ = std::min(spec_bps_, c0);
-    if (xc > 0) spec_xd_ = xf + xc;
+    spec_push(p, w, overlap, nullptr);
+}
+
+// ---- fused first stage (K6, k_fused.cu) ------------------------------------
+bool Store::can_fuse(const Operator& op, i64 s) {
+    // Opt-in (KRY_FUSED_PASS=1): measured slower than the separate kernels
+    // on B200 ("fused first-stage pass").
+    const bool on = [] {
+        const char* e = std::getenv("KRY_FUSED_PASS");
+        return e && std::atoi(e) == 1;
+    }();
+    if (!on || !can_speculate(s + 1) || op.kind != Operator::LAPLACE2D || ctx_.nranks != 1 || op.nloc != n_) return false;
+    for (auto& b : fraw_) b.ensure(static_cast<size_t>(ld_) * (s + 1) * 8);
+    ctx_.gram_partials.ensure(static_cast<size_t>(std::max(fused_partials_doubles(), gram_scratch_doubles(s + 1))) * 8);
+    return fused_pass_supported(op.geom, static_cast<int>(s), s + 1, max_cols_ - (s + 1), ld_, q_.p, fraw_[0].p,
+                                fraw_[1].p);
+}
+
+void Store::spec_fused_first(Operator& op, i64 s, bool overlap) {
+    const i64 w = s + 1;
+    const SpecPlan p = spec_plan(w, overlap);
+    const int buf = 0;
+    double* raw = fraw_[buf].p;
+    // raw block: column 0 = the start (store column c0), 1..s = A^k·start
+    KB_CUDA(cudaMemcpyAsync(raw, col(p.c0), static_cast<size_t>(n_) * 8, cudaMemcpyDeviceToDevice, ctx_.stream));
+    cudaEvent_t t0 = ctx_.begin_phase();
+    if (!op.mpk(raw, raw + ld_, ld_, static_cast<int>(s)))
+        for (i64 k = 0; k < s; ++k) op.apply(raw + k * ld_, raw + (k + 1) * ld_);
+    ctx_.end_phase(PH_MPK, t0);
+    std::vector<int> tiles;
+    cudaEvent_t t1 = ctx_.begin_phase();
+    launch_gram_pass(ctx_.stream, n_, p.c0 > 0 ? col(0) : nullptr, ld_, p.c0, raw, ld_, w, true,
+                     ctx_.gram_partials.p, ctx_.gram_packed.p, tiles, ctx_.launches, p.xf, p.xc);
+    ctx_.end_phase(PH_GRAM, t1);
+    ctx_.gram_bytes += 8.0 * n_ * (p.c0 + w);
+    ctx_.gram_launches += 1;
+    const PipBlockArgs a = spec_factor(p, w);
+    fpend_ = {true, p.c0, w, buf, a.coef, a.skip};
+    spec_push(p, w, overlap, raw);
+}
+
+void Store::spec_fused_next(Operator& op, i64 s) {
+    const i64 w = s + 1;
+    if (!fpend_.live || fpend_.w != w) fail(KRY_INTERNAL, "fused pass without a pending block");
+    const SpecPlan p = spec_plan(w, true);
+    const int nbuf = 1 - fpend_.buf;
+    FusedPassArgs f{};
+    f.Q = q_.p;
+    f.ld = ld_;
+    f.V = fraw_[fpend_.buf].p;
+    f.Vn = fraw_[nbuf].p;
+    f.c0 = static_cast<int>(fpend_.c0);
+    f.w = static_cast<int>(w);
+    f.coef = fpend_.coef;
+    f.skip = fpend_.skip;
+    f.c0n = static_cast<int>(p.c0);
+    f.x_first = static_cast<int>(p.xf);
+    f.x_count = static_cast<int>(p.xc);
+    f.partials = ctx_.gram_partials.p;
+    cudaEvent_t t0 = ctx_.begin_phase();
+    launch_fused_pass(ctx_.stream, op.geom, static_cast<int>(s), f, ctx_.gram_packed.p, ctx_.launches);
+    ctx_.end_phase(PH_FUSED, t0);
+    // necessary HBM traffic: prefix + raw block read once, block j and raw block j+1 written
+    ctx_.fused_bytes += 8.0 * n_ * (fpend_.c0 + 3.0 * w);
+    ctx_.fused_launches += 1;
+    const PipBlockArgs a = spec_factor(p, w);
+    fpend_ = {true, p.c0, w, nbuf, a.coef, a.skip};
+    spec_push(p, w, true, fraw_[nbuf].p);
+}
+
+void Store::spec_flush() {
+    if (!fpend_.live) return;
+    const i64 c0 = fpend_.c0, w = fpend_.w;
+    cudaEvent_t t1 = ctx_.begin_phase();
+    launch_update(ctx_.stream, n_, c0 > 0 ? col(0) : nullptr, ld_, c0, fraw_[fpend_.buf].p, ld_, w, fpend_.coef, true,
+                  col(c0), ld_, ctx_.launches, fpend_.skip);
+    ctx_.end_phase(PH_UPDATE, t1);
+    ctx_.update_bytes += 8.0 * n_ * (c0 + 2.0 * w);
+    ctx_.update_launches += 1;
+    fpend_.live = false;
 }
 
 i64 Store::resolve_speculative(Sync& sync) {
@@ -174,6 +268,11 @@ i64 Store::resolve_speculative(Sync& sync) {
         const double* slot = spec_host_.p + i * kSlotDoubles;
         if (slot[kSlotStatus] != 0.0) {
             failed = static_cast<i64>(i);
+            // fused path: the block's raw columns live outside the store;
+            // put them where the synchronous redo expects them
+            if (b.raw)
+                KB_CUDA(cudaMemcpy2DAsync(col(b.c0), ld_ * 8, b.raw, ld_ * 8, n_ * 8, b.w, cudaMemcpyDeviceToDevice,
+                                          ctx_.stream));
             break;
         }
         OrthoRes res;

@@ -80,6 +80,15 @@ public:
     // redoes it on the synchronous path) or −1.
     bool can_speculate(i64 w) const;
     void preprocess_speculative(i64 w, bool overlap);
+    // Fused first stage (K6, 2-D stencil, one rank): the queue's first block
+    // runs MPK → Gram → factorisation into a raw buffer outside the store
+    // and leaves its update pending; every later block is one fused pass
+    // (pending update → MPK → Gram, k_fused.cu) + factorisation;
+    // spec_flush() runs the last pending update (before resolve).
+    bool can_fuse(const Operator& op, i64 s);
+    void spec_fused_first(Operator& op, i64 s, bool overlap);
+    void spec_fused_next(Operator& op, i64 s);
+    void spec_flush();
     i64 resolve_speculative(Sync& sync);
     i64 spec_filled() const { return spec_.empty() ? filled_ : spec_filled_; }
     bool spec_panel_full() const;
@@ -117,7 +126,23 @@ private:
         i64 c0, w;
         bool overlap;
         i64 x_first, x_count;
+        const double* raw;  // raw block outside the store (fused path) or nullptr
     };
+    struct SpecPlan {
+        i64 c0, idx, xf, xc;
+    };
+    SpecPlan spec_plan(i64 w, bool overlap);
+    PipBlockArgs spec_factor(const SpecPlan& p, i64 w);
+    void spec_push(const SpecPlan& p, i64 w, bool overlap, const double* raw);
+    struct FusedPending {
+        bool live = false;
+        i64 c0 = 0, w = 0;
+        int buf = 0;
+        double* coef = nullptr;
+        int* skip = nullptr;
+    };
+    FusedPending fpend_;
+    DevBuf fraw_[2];  // raw blocks of the fused path (double-buffered)
     std::vector<SpecBlock> spec_;
     i64 spec_filled_ = 0, spec_bps_ = 0, spec_xd_ = 0;
     DevBuf spec_slots_, spec_coef_, spec_skip_;

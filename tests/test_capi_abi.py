@@ -38,7 +38,7 @@ def test_library_exports_every_declared_symbol():
 
 
 def test_abi_version_and_config_defaults(kb):
-    assert kb.lib().kry_abi_version() == 1
+    assert kb.lib().kry_abi_version() == 2
     c = kb._capi.kry_solver_config()
     kb.lib().kry_solver_config_default(C.byref(c))
     # krylov::SolverConfig defaults (gmres.hpp:18-24)

@@ -70,6 +70,19 @@ def test_solver_matches_reference(kb, ctx, ref, key):
     assert_parity(rep, g)
 
 
+# The opt-in fused first-stage pass (K6, k_fused.cu: block j's update, block
+# j+1's MPK and Gram in one kernel) on every two-stage 2-D stencil golden.
+@pytest.mark.parametrize("key", sorted(k for k in GOLDEN if GOLDEN[k]["operator"] != "csr"
+                                       and GOLDEN[k]["dims"] == 2 and not GOLDEN[k]["standard"]
+                                       and GOLDEN[k]["kind"] == 3))
+def test_solver_matches_reference_fused_pass(kb, ctx, ref, monkeypatch, key):
+    monkeypatch.setenv("KRY_FUSED_PASS", "1")
+    rep, g = run_golden(kb, ref, key)
+    assert_parity(rep, g)
+    if g["shat"] > 5 or g["shat"] == 0:  # a big panel of ≥ 2 blocks: the fused kernel ran
+        assert rep.telemetry["fused_launches"] > 0
+
+
 # The golden grids are below the fused-MPK size heuristic; run the 2-D
 # stencil configurations again with the fused one-pass MPK forced on.
 @pytest.mark.parametrize("key", sorted(k for k in GOLDEN if GOLDEN[k]["operator"] != "csr"

@@ -55,7 +55,8 @@ def parse():
     p.add_argument("--global-grid", type=int, default=0,
                    help="strong scaling: fixed global grid side (e.g. 8000 = BASELINE configs[2]) split over the ranks")
     p.add_argument("--shat", type=int, default=60)
-    p.add_argument("--scheme", choices=["two-stage", "bcgs-pip2"], default="two-stage")
+    p.add_argument("--scheme", choices=["two-stage", "bcgs-pip2", "standard"], default="two-stage",
+                   help="standard = standard_gmres (gmres.hpp:404: s = 1, CGS2), the paper's GMRES column")
     p.add_argument("--tts", action="store_true", help="also run a full solve from x0 = 0 at the bench grid")
     p.add_argument("--no-tts512", action="store_true", help="skip the 512² time-to-solution solves")
     p.add_argument("--no-cpu-baseline", action="store_true")
@@ -287,6 +288,9 @@ def run_ours(args):
         shape = f"3D Laplace 7-pt {nx}x{ny}x{nz}"
     n = op.n
     kind = kb.OrthoKind.TWO_STAGE if args.scheme == "two-stage" else kb.OrthoKind.BCGS_PIP2
+    std = args.scheme == "standard"
+    solve_dev = kb.standard_gmres_device if std else kb.sstep_gmres_device
+    solve_host = kb.lib().kry_standard_gmres if std else kb.lib().kry_sstep_gmres
     cfg_cycle = kb.SolverConfig(scheme=kb.OrthoScheme(kind, args.shat), big_step=args.shat if kind == 3 else 0,
                                 max_iters=60)
     ones = torch.ones(n, dtype=torch.float64, device="cuda")
@@ -301,7 +305,7 @@ def run_ours(args):
             dist.barrier()
 
     def cycle():
-        return kb.sstep_gmres_device(op, b.data_ptr(), x.data_ptr(), cfg_cycle, x.data_ptr())
+        return solve_dev(op, b.data_ptr(), x.data_ptr(), cfg_cycle, x.data_ptr())
 
     for _ in range(args.warmup):
         cycle()
@@ -352,8 +356,7 @@ def run_ours(args):
         ccfg = cfg_cycle.to_c()
         def host_cycle():
             rep_c, cyc, pb, pbp = kb._new_report(1024)
-            kb._check(kb.lib().kry_sstep_gmres(ctx.handle, op.handle, P(hb), P(hx), C.byref(ccfg), C.byref(rep_c),
-                                               P(hx)))
+            kb._check(solve_host(ctx.handle, op.handle, P(hb), P(hx), C.byref(ccfg), C.byref(rep_c), P(hx)))
             return rep_c.ortho_bytes
 
         for _ in range(args.warmup):  # the first host-buffer call sizes the upload buffers
@@ -438,7 +441,7 @@ def run_ours(args):
         cfg_full = kb.SolverConfig(scheme=kb.OrthoScheme(kind, args.shat), big_step=args.shat if kind == 3 else 0)
         barrier()
         t0 = time.perf_counter()
-        rep = kb.sstep_gmres_device(op, b.data_ptr(), None, cfg_full, x.data_ptr())
+        rep = solve_dev(op, b.data_ptr(), None, cfg_full, x.data_ptr())
         barrier()
         t_tts = allred([time.perf_counter() - t0], MAX)[0]
         tts = {"seconds": t_tts, "status": rep.status.name.lower(), "iterations": rep.iterations,
@@ -452,11 +455,13 @@ def run_ours(args):
             "warmup": args.warmup, "ms_per_step": 1e3 * t_el / steps, "higher_is_better": True,
             "scaling": "strong" if strong else "weak",
             "vs_baseline": None, "dtype": "f64", "data": "synthetic (b = A*1, x0 = 0, then warm restarts)",
-            "config": {"workload": f"{shape} ({n} rows per GPU), s-step GMRES(60) s=5, "
-                                   f"{args.scheme} BlkOrtho shat={args.shat}",
+            "config": {"workload": f"{shape} ({n} rows per GPU), " + (
+                           "standard GMRES(60) (s = 1, CGS2 as BCGS2-CholQR2)" if std else
+                           f"s-step GMRES(60) s=5, {args.scheme} BlkOrtho shat={args.shat}"),
                        "grid": [nx, ny] if args.dims == 2 else [nx, ny, nz], "rows_per_gpu": n, "m": 60, "s": 5,
                        "shat": args.shat,
-                       "step": "one full restart cycle (60 iterations) through kry_sstep_gmres_device",
+                       "step": "one full restart cycle (60 iterations) through kry_" +
+                               ("standard" if std else "sstep") + "_gmres_device",
                        "parallelism": f"row-partitioned dp{world}", "l2": "inputs larger than L2 (basis 8*61*n B)"},
             "roofline": {"bound": "hbm", "kernel": dom, "achieved": achieved, "peak": peak, "unit": "GB/s",
                          "frac": achieved / peak, "traffic": traffic, "peak_source": peak_src,

@@ -262,6 +262,8 @@ int kry_standard_gmres(kry_ctx* ctx, kry_operator* op, const double* b, const do
 /* Inputs already resident in HBM (d_x0 may be NULL; d_x_out may be NULL). */
 int kry_sstep_gmres_device(kry_ctx* ctx, kry_operator* op, const double* d_b, const double* d_x0,
                            const kry_solver_config* cfg, kry_report* report, double* d_x_out);
+int kry_standard_gmres_device(kry_ctx* ctx, kry_operator* op, const double* d_b, const double* d_x0,
+                              const kry_solver_config* cfg, kry_report* report, double* d_x_out);
 
 #ifdef __cplusplus
 }

@@ -657,12 +657,22 @@ def standard_gmres(op: Operator, b, x0, cfg: SolverConfig) -> SolveReport:
     return _solve(lib().kry_standard_gmres, op, b, x0, cfg)
 
 
+def _solve_device(fn, op: Operator, d_b: int, d_x0: Optional[int], cfg: SolverConfig,
+                  d_x_out: Optional[int]) -> SolveReport:
+    rep, cyc, pb, pbp = _new_report()
+    c = cfg.to_c()
+    _check(fn(op.ctx.handle, op.handle, C.c_void_p(d_b), C.c_void_p(d_x0) if d_x0 else None, C.byref(c),
+              C.byref(rep), C.c_void_p(d_x_out) if d_x_out else None))
+    return _report_from_c(rep, cyc, pb, pbp, None)
+
+
 def sstep_gmres_device(op: Operator, d_b: int, d_x0: Optional[int], cfg: SolverConfig,
                        d_x_out: Optional[int] = None) -> SolveReport:
     """Inputs already resident in HBM (raw device pointers, e.g. tensor.data_ptr())."""
-    rep, cyc, pb, pbp = _new_report()
-    c = cfg.to_c()
-    _check(lib().kry_sstep_gmres_device(op.ctx.handle, op.handle, C.c_void_p(d_b),
-                                        C.c_void_p(d_x0) if d_x0 else None, C.byref(c), C.byref(rep),
-                                        C.c_void_p(d_x_out) if d_x_out else None))
-    return _report_from_c(rep, cyc, pb, pbp, None)
+    return _solve_device(lib().kry_sstep_gmres_device, op, d_b, d_x0, cfg, d_x_out)
+
+
+def standard_gmres_device(op: Operator, d_b: int, d_x0: Optional[int], cfg: SolverConfig,
+                          d_x_out: Optional[int] = None) -> SolveReport:
+    """standard_gmres (gmres.hpp:404) with inputs resident in HBM."""
+    return _solve_device(lib().kry_standard_gmres_device, op, d_b, d_x0, cfg, d_x_out)

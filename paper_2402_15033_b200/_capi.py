@@ -121,6 +121,7 @@ SIGNATURES = {
     "kry_sstep_gmres": (C.c_int, [vp, vp, P_dbl, P_dbl, C.POINTER(kry_solver_config), C.POINTER(kry_report), P_dbl]),
     "kry_standard_gmres": (C.c_int, [vp, vp, P_dbl, P_dbl, C.POINTER(kry_solver_config), C.POINTER(kry_report), P_dbl]),
     "kry_sstep_gmres_device": (C.c_int, [vp, vp, vp, vp, C.POINTER(kry_solver_config), C.POINTER(kry_report), vp]),
+    "kry_standard_gmres_device": (C.c_int, [vp, vp, vp, vp, C.POINTER(kry_solver_config), C.POINTER(kry_report), vp]),
 }
 
 _lib = None

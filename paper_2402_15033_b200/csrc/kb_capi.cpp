@@ -752,4 +752,9 @@ int kry_sstep_gmres_device(kry_ctx* ctx, kry_operator* op, const double* d_b, co
     return solve_common(ctx, op, d_b, d_x0, cfg, report, d_x_out, true, false);
 }
 
+int kry_standard_gmres_device(kry_ctx* ctx, kry_operator* op, const double* d_b, const double* d_x0,
+                              const kry_solver_config* cfg, kry_report* report, double* d_x_out) {
+    return solve_common(ctx, op, d_b, d_x0, cfg, report, d_x_out, true, true);
+}
+
 }  // extern "C"

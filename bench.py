@@ -422,7 +422,11 @@ def run_ours(args):
         kb.lib().kry_spmv_device(ctx.handle, op5.handle, one5.data_ptr(), b5.data_ptr())
         tts512 = {"grid": [512, 512], "rel_tol": 1e-6,
                   "cpu_reference_seconds_survey": {"bcgs_pip2_1thread": 329.5, "two_stage_8threads": 239.4,
-                                                   "source": "BASELINE.md §2 (survey container, 8-core Xeon)"}}
+                                                   "source": "BASELINE.md §2 (survey container, 8-core Xeon)"},
+                  "cpu_reference_seconds_gpu_box": {"two_stage_1thread": 202.3, "two_stage_16threads": 157.7,
+                                                    "bcgs_pip2_1thread": 198.1, "bcgs_pip2_16threads": 203.8,
+                                                    "source": "profiles/cpu_ref_tts_512.jsonl (tools/cpu_ref_tts.py "
+                                                              "on a B200 box host, 16 cores, round 1)"}}
         for label, knd, sh in [("bcgs_pip2", kb.OrthoKind.BCGS_PIP2, 0), ("two_stage_shat60", kb.OrthoKind.TWO_STAGE, 60)]:
             cfgf = kb.SolverConfig(scheme=kb.OrthoScheme(knd, sh), big_step=sh)
             kb.sstep_gmres_device(op5, b5.data_ptr(), None, cfgf, x5.data_ptr())  # warm (module load, workspace)

@@ -83,6 +83,7 @@ struct FusedMaps {
 template <int S, int WMAX, int NB, int NX>
 __global__ void __launch_bounds__(kFuThreads, 1)
     fused_pass_kernel(const __grid_constant__ FusedMaps maps, const FusedPassArgs a, int nslots) {
+    KB_PDL_WAIT();
     if (a.skip && *a.skip) return;  // block j's factorisation failed: nothing may change (k_pip.cu)
     constexpr int H = (S + 1) & ~1, STEP = 64 - 2 * H;
     static_assert(STEP % 4 == 0, "core columns must split into 4-row DMMA chunks");
@@ -484,7 +485,7 @@ void launch_fused_pass(cudaStream_t stream, const StencilGeom& g, int s, FusedPa
     const int grid = static_cast<int>(std::max<i64>(1, std::min<i64>(sms, a.ntasks)));
     if (static_cast<i64>(grid) * T * 64 > fused_partials_doubles()) fail(KRY_INTERNAL, "fused pass partials");
     void* args[] = {&maps, &a, &nslots};
-    KB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(kFuThreads), args, smem, stream));
+    launch_pdl_c(fn, dim3(grid), dim3(kFuThreads), smem, stream, args);
     KB_LAUNCHED();
     launch_gram_reduce(stream, a.partials, grid, T * 64, d_packed);
     launches += 2;

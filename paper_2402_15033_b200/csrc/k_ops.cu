@@ -21,6 +21,7 @@
 #include <type_traits>
 
 #include "kb_common.hpp"
+#include "kb_device.hpp"
 #include "kb_kernels.hpp"
 
 namespace kb {
@@ -77,6 +78,7 @@ __global__ void __launch_bounds__(kBlock) stencil_kernel(const StencilGeom g, co
                                                          const double* __restrict__ b,
                                                          double* __restrict__ y,
                                                          double* __restrict__ partials) {
+    KB_PDL_WAIT();
     const i64 ix = blockIdx.x * static_cast<i64>(kBlock) + threadIdx.x;
     const i64 nx = g.nx;
     double sq = 0.0;
@@ -159,6 +161,7 @@ __global__ void __launch_bounds__(kBlock) stencil2d_vec_kernel(const StencilGeom
                                                                const double* __restrict__ b,
                                                                double* __restrict__ y,
                                                                double* __restrict__ partials) {
+    KB_PDL_WAIT();
     const i64 ix = 2 * (blockIdx.x * static_cast<i64>(kBlock) + threadIdx.x);
     const i64 nx = g.nx;
     const bool active = ix < nx;
@@ -238,6 +241,7 @@ __global__ void __launch_bounds__(kBlock, 6) stencil3d_vec_kernel(const StencilG
                                                                   const double* __restrict__ b,
                                                                   double* __restrict__ y,
                                                                   double* __restrict__ partials) {
+    KB_PDL_WAIT();
     const int nx = static_cast<int>(g.nx), ny = static_cast<int>(g.ny), half = nx / 2;
     const i64 plane = g.nx * g.ny;
     const int q = blockIdx.x * kBlock + threadIdx.x;  // pair index inside a plane
@@ -425,6 +429,7 @@ __global__ void __launch_bounds__(kBlock, 2) mpk2d_kernel(const StencilGeom g, c
                                                        const double* __restrict__ halo_hi,
                                                        double* __restrict__ out, i64 ldo, i64 nwx, i64 band,
                                                        i64 ntasks) {
+    KB_PDL_WAIT();
     const int lane = threadIdx.x & 31;
     const i64 nwarps = static_cast<i64>(gridDim.x) * (kBlock / 32);
     for (i64 task = blockIdx.x * static_cast<i64>(kBlock / 32) + (threadIdx.x >> 5); task < ntasks;
@@ -458,6 +463,7 @@ __global__ void __launch_bounds__(kBlock) csr_warp_kernel(i64 nloc, const RP* __
                                                           const double* __restrict__ x,
                                                           const double* __restrict__ b, double* __restrict__ y,
                                                           double* __restrict__ partials, double* part_sum) {
+    KB_PDL_WAIT();
     __shared__ double s_prod[kBlock / 32][kCsrChunk];
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const i64 stride = static_cast<i64>(gridDim.x) * (kBlock / 32) * 32;
@@ -514,6 +520,7 @@ __global__ void __launch_bounds__(kBlock) csr_warp_kernel(i64 nloc, const RP* __
 
 __global__ void __launch_bounds__(kBlock) finalize_kernel(const double* __restrict__ partials, int count,
                                                           double* __restrict__ out) {
+    KB_PDL_WAIT();
     double s = 0.0;
     for (int i = threadIdx.x; i < count; i += blockDim.x) s += partials[i];
     const double t = block_sum(s);
@@ -522,6 +529,7 @@ __global__ void __launch_bounds__(kBlock) finalize_kernel(const double* __restri
 
 __global__ void __launch_bounds__(kBlock) scale_div_kernel(i64 n, const double* __restrict__ r, double gamma,
                                                            double* __restrict__ out) {
+    KB_PDL_WAIT();
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
         out[i] = r[i] / gamma;
 }
@@ -529,6 +537,7 @@ __global__ void __launch_bounds__(kBlock) scale_div_kernel(i64 n, const double* 
 __global__ void __launch_bounds__(kBlock) xupdate_kernel(i64 n, const double* __restrict__ x,
                                                          const double* __restrict__ q, i64 ldq, int k,
                                                          const Coef64 y, double* __restrict__ xnew) {
+    KB_PDL_WAIT();
     for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x) {
         double s = x[i];
         for (int l = 0; l < k; ++l) s = fma(y.v[l], q[i + l * ldq], s);
@@ -584,9 +593,9 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
         dim3 grid = stencil_grid(g);
         grid.x = static_cast<unsigned>(ceil_div(g.nx / 2, kBlock));
         if (b)
-            stencil2d_vec_kernel<true><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+            launch_pdl(stencil2d_vec_kernel<true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
         else
-            stencil2d_vec_kernel<false><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+            launch_pdl(stencil2d_vec_kernel<false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
         KB_LAUNCHED();
         ++launches;
         return b ? static_cast<int>(grid.x * grid.y) : 0;
@@ -598,9 +607,9 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
     if (vec3 && g.dims == 3 && (g.nx & 1) == 0 && g.nx * g.ny < (i64(1) << 30) && g.nzl < (i64(1) << 30) && a16(x) && a16(y) && a16(b) && a16(halo_lo) && a16(halo_hi)) {
         const dim3 grid = stencil3d_vec_grid(g);
         if (b)
-            stencil3d_vec_kernel<true><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+            launch_pdl(stencil3d_vec_kernel<true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
         else
-            stencil3d_vec_kernel<false><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+            launch_pdl(stencil3d_vec_kernel<false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
         KB_LAUNCHED();
         ++launches;
         return b ? static_cast<int>(grid.x * grid.y) : 0;
@@ -608,14 +617,14 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
     const dim3 grid = stencil_grid(g);
     if (g.dims == 2) {
         if (b)
-            stencil_kernel<2, true><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+            launch_pdl(stencil_kernel<2, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
         else
-            stencil_kernel<2, false><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+            launch_pdl(stencil_kernel<2, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
     } else {
         if (b)
-            stencil_kernel<3, true><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+            launch_pdl(stencil_kernel<3, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
         else
-            stencil_kernel<3, false><<<grid, kBlock, 0, s>>>(g, x, halo_lo, halo_hi, b, y, partials);
+            launch_pdl(stencil_kernel<3, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
     }
     KB_LAUNCHED();
     ++launches;
@@ -675,7 +684,7 @@ void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const 
         const i64 ntasks = nwx * ceil_div(g.lines, band);
         const unsigned grid = static_cast<unsigned>(
             std::min<i64>(ceil_div(ntasks, kBlock / 32), static_cast<i64>(num_sms()) * std::max(per_sm, 1)));
-        kernel<<<grid, kBlock, 0, st>>>(g, x, halo_lo, halo_hi, out, ldo, nwx, band, ntasks);
+        launch_pdl(kernel, grid, kBlock, 0, st, g, x, halo_lo, halo_hi, out, ldo, nwx, band, ntasks);
     };
     switch (s) {
         case 1: go(mpk2d_kernel<1>); break;
@@ -699,11 +708,9 @@ int launch_csr(cudaStream_t s, i64 nloc, const int64_t* row_ptr, const int32_t* 
     const int grid = b ? reduce_grid()
                        : static_cast<int>(std::max<i64>(1, std::min<i64>(ceil_div(warps, kBlock / 32), i64(1) << 30)));
     if (b)
-        csr_warp_kernel<CSR_ONLY, true, int64_t>
-            <<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials, nullptr);
+        launch_pdl(csr_warp_kernel<CSR_ONLY, true, int64_t>, grid, kBlock, 0, s, nloc, row_ptr, col, vals, x, b, y, partials, nullptr);
     else
-        csr_warp_kernel<CSR_ONLY, false, int64_t>
-            <<<grid, kBlock, 0, s>>>(nloc, row_ptr, col, vals, x, b, y, partials, nullptr);
+        launch_pdl(csr_warp_kernel<CSR_ONLY, false, int64_t>, grid, kBlock, 0, s, nloc, row_ptr, col, vals, x, b, y, partials, nullptr);
     KB_LAUNCHED();
     ++launches;
     return b ? grid : 0;
@@ -719,17 +726,13 @@ int launch_csr_sliced(cudaStream_t s, i64 nloc, int nslices, const int32_t* cons
         const bool first = p == 0, lastp = p == nslices - 1;
         const int grid = (b && lastp) ? reduce_grid() : grid_free;
         if (first)
-            csr_warp_kernel<CSR_FIRST, false, int32_t>
-                <<<grid, kBlock, 0, s>>>(nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
+            launch_pdl(csr_warp_kernel<CSR_FIRST, false, int32_t>, grid, kBlock, 0, s, nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
         else if (!lastp)
-            csr_warp_kernel<CSR_MID, false, int32_t>
-                <<<grid, kBlock, 0, s>>>(nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
+            launch_pdl(csr_warp_kernel<CSR_MID, false, int32_t>, grid, kBlock, 0, s, nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
         else if (b)
-            csr_warp_kernel<CSR_LAST, true, int32_t>
-                <<<grid, kBlock, 0, s>>>(nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
+            launch_pdl(csr_warp_kernel<CSR_LAST, true, int32_t>, grid, kBlock, 0, s, nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
         else
-            csr_warp_kernel<CSR_LAST, false, int32_t>
-                <<<grid, kBlock, 0, s>>>(nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
+            launch_pdl(csr_warp_kernel<CSR_LAST, false, int32_t>, grid, kBlock, 0, s, nloc, row_ptr[p], col[p], vals[p], x, b, y, partials, part_sum);
         KB_LAUNCHED();
         ++launches;
     }
@@ -738,21 +741,21 @@ int launch_csr_sliced(cudaStream_t s, i64 nloc, int nslices, const int32_t* cons
 
 void launch_finalize_sum(cudaStream_t s, const double* partials, int count, double* out,
                          int64_t& launches) {
-    finalize_kernel<<<1, kBlock, 0, s>>>(partials, count, out);
+    launch_pdl(finalize_kernel, 1, kBlock, 0, s, partials, count, out);
     KB_LAUNCHED();
     ++launches;
 }
 
 void launch_scale_div(cudaStream_t s, i64 n, const double* r, double gamma, double* out,
                       int64_t& launches) {
-    scale_div_kernel<<<grid_for(n), kBlock, 0, s>>>(n, r, gamma, out);
+    launch_pdl(scale_div_kernel, grid_for(n), kBlock, 0, s, n, r, gamma, out);
     KB_LAUNCHED();
     ++launches;
 }
 
 void launch_xupdate(cudaStream_t s, i64 n, const double* x, const double* Q, i64 ldq, int k,
                     const Coef64& y, double* xnew, int64_t& launches) {
-    xupdate_kernel<<<grid_for(n), kBlock, 0, s>>>(n, x, Q, ldq, k, y, xnew);
+    launch_pdl(xupdate_kernel, grid_for(n), kBlock, 0, s, n, x, Q, ldq, k, y, xnew);
     KB_LAUNCHED();
     ++launches;
 }

@@ -14,6 +14,7 @@
 #include <cuda_runtime.h>
 
 #include "kb_common.hpp"
+#include "kb_device.hpp"
 #include "kb_kernels.hpp"
 
 namespace kb {
@@ -24,6 +25,7 @@ constexpr int kPipThreads = 256;
 constexpr int kPipMaxC0 = 64, kPipMaxW = 8;
 
 __global__ void __launch_bounds__(kPipThreads) pip_block_kernel(const PipBlockArgs a) {
+    KB_PDL_WAIT();
     __shared__ double rc[kPipMaxC0 * kPipMaxW];  // R_col, column-major c0 × w
     __shared__ double s[kPipMaxW * kPipMaxW];    // G, then S = G − R_colᵀR_col
     __shared__ double r[kPipMaxW * kPipMaxW];    // R_jj (upper), column-major
@@ -142,7 +144,7 @@ __global__ void __launch_bounds__(kPipThreads) pip_block_kernel(const PipBlockAr
 
 void launch_pip_block(cudaStream_t stream, const PipBlockArgs& a, int64_t& launches) {
     if (a.c0 > kPipMaxC0 || a.w > kPipMaxW || a.w < 1) fail(KRY_INTERNAL, "speculative block shape");
-    pip_block_kernel<<<1, kPipThreads, 0, stream>>>(a);
+    launch_pdl(pip_block_kernel, 1, kPipThreads, 0, stream, a);
     KB_LAUNCHED();
     launches += 1;
 }

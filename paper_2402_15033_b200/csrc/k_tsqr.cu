@@ -156,6 +156,7 @@ template <int NBW, int NB, int NX = 0, int CW = consumer_warps(NBW)>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
     gram_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_p,
                 const TsParams p, double* __restrict__ partials) {
+    KB_PDL_WAIT();
     constexpr int T = tile_count(NBW, NB) + NX * (NB - NBW);
     extern __shared__ __align__(1024) unsigned char smem[];
     uint64_t *full, *empty;
@@ -258,6 +259,7 @@ __global__ void __launch_bounds__((CW + 1) * 32, 1)
 // stride, then a fixed xor tree.  Deterministic for a given grid size.
 __global__ void gram_reduce_kernel(const double* __restrict__ partials, int grid, int per_cta,
                                    double* __restrict__ packed) {
+    KB_PDL_WAIT();
     const int gw = (blockIdx.x * blockDim.x + threadIdx.x) >> 5;
     const int lane = threadIdx.x & 31;
     if (gw >= per_cta) return;
@@ -308,6 +310,7 @@ template <int WMAX, int R>
 __global__ void __launch_bounds__(256)
     update_kernel(i64 n, const double* __restrict__ P, i64 ldp, int cp, const double* V, i64 ldv, int w,
                   const double* __restrict__ coef, int triangular, double* out, i64 ldo, const int* skip) {
+    KB_PDL_WAIT();
     if (skip && *skip) return;  // speculative block whose factorisation failed (k_pip.cu)
     // Columns w ≤ j < WMAX are identity padding (zero coefficients, inv = 1):
     // the arithmetic below is branch-free and leaves them at zero.
@@ -339,6 +342,7 @@ __global__ void __launch_bounds__(256)
 __global__ void __launch_bounds__(256)
     update_pair_kernel(i64 n, const double* __restrict__ P, i64 ldp, int cp, const double* V, i64 ldv, int w,
                        const double* __restrict__ coef, int triangular, double* out, i64 ldo, const int* skip) {
+    KB_PDL_WAIT();
     if (skip && *skip) return;
     constexpr int H = 32;
     extern __shared__ __align__(16) double c_sm[];
@@ -417,6 +421,7 @@ template <int NBW, int NB, int CW = 8>
 __global__ void __launch_bounds__((CW + 1) * 32, 1)
     update_mma_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_p,
                       const TsParams p, const double* __restrict__ mfrag, double* out, i64 ldo) {
+    KB_PDL_WAIT();
     constexpr int KC = 2 * NB;
     extern __shared__ __align__(1024) unsigned char smem[];
     uint64_t *full, *empty;
@@ -485,6 +490,7 @@ __global__ void __launch_bounds__(9 * 32, 1)
     update_tma_kernel(const __grid_constant__ CUtensorMap map_v, const __grid_constant__ CUtensorMap map_p,
                       i64 n, int cp, int w, const double* __restrict__ coef, double* out, i64 ldo,
                       const int* skip) {
+    KB_PDL_WAIT();
     if (skip && *skip) return;  // speculative block whose factorisation failed (k_pip.cu)
     constexpr int CW = 8, BOX = kTmaRows, TR = BOX * R;
     extern __shared__ __align__(1024) unsigned char smem[];
@@ -778,8 +784,8 @@ size_t ring_bytes(const TsParams& p) {
 }  // namespace
 
 void launch_gram_reduce(cudaStream_t stream, const double* partials, int grid, int per_cta, double* packed) {
-    gram_reduce_kernel<<<ceil_div(static_cast<i64>(per_cta) * 32, 256), 256, 0, stream>>>(partials, grid, per_cta,
-                                                                                          packed);
+    launch_pdl(gram_reduce_kernel, static_cast<unsigned>(ceil_div(static_cast<i64>(per_cta) * 32, 256)), 256, 0, stream,
+               partials, grid, per_cta, packed);
     KB_LAUNCHED();
 }
 void set_kernel_smem(const void* kernel, size_t bytes) { set_smem(kernel, bytes); }
@@ -839,10 +845,11 @@ void launch_gram_pass(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 
     if (!fn) fail(KRY_UNSUPPORTED, "gram shape");
     set_smem(fn, smem);
     void* args[] = {&mv, &mp, &p, &d_partials};
-    KB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3((cw + 1) * 32), args, smem, stream));
+    launch_pdl_c(fn, dim3(grid), dim3((cw + 1) * 32), smem, stream, args);
     KB_LAUNCHED();
     const int per_cta = T * 64;
-    gram_reduce_kernel<<<ceil_div(per_cta * 32, 256), 256, 0, stream>>>(d_partials, grid, per_cta, d_packed);
+    launch_pdl(gram_reduce_kernel, static_cast<unsigned>(ceil_div(per_cta * 32, 256)), 256, 0, stream, d_partials, grid,
+               per_cta, d_packed);
     KB_LAUNCHED();
     launches += 2;
 }
@@ -864,7 +871,7 @@ void launch_update_mma(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64
     if (!fn) fail(KRY_UNSUPPORTED, "update_mma shape");
     set_smem(fn, smem);
     void* args[] = {&mv, &mp, &p, &d_mfrag, &out, &ldo};
-    KB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(9 * 32), args, smem, stream));
+    launch_pdl_c(fn, dim3(grid), dim3(9 * 32), smem, stream, args);
     KB_LAUNCHED();
     launches += 1;
 }
@@ -907,7 +914,7 @@ static bool launch_update_tma(cudaStream_t stream, i64 n, const double* P, i64 l
     set_smem(fn, smem);
     int cpi = static_cast<int>(cp), wi = static_cast<int>(w);
     void* args[] = {&mv, &mp, &n, &cpi, &wi, const_cast<double**>(&d_coef), &out, &ldo, const_cast<int**>(&skip)};
-    KB_CUDA(cudaLaunchKernel(fn, dim3(grid), dim3(9 * 32), args, smem, stream));
+    launch_pdl_c(fn, dim3(grid), dim3(9 * 32), smem, stream, args);
     KB_LAUNCHED();
     launches += 1;
     return true;
@@ -942,7 +949,7 @@ void launch_update(cudaStream_t stream, i64 n, const double* P, i64 ldp, i64 cp,
         const int per_sm = occupancy(reinterpret_cast<const void*>(kernel), 256, smem);
         const i64 want = ceil_div(n, (wmax == 64 ? 128 : 256) * rows_per_thread);
         const int grid = static_cast<int>(std::max<i64>(1, std::min<i64>(want, static_cast<i64>(sm_count()) * std::max(per_sm, 1))));
-        kernel<<<grid, 256, smem, stream>>>(n, P, ldp, static_cast<int>(cp), V, ldv, static_cast<int>(w), d_coef,
+        launch_pdl(kernel, grid, 256, smem, stream, n, P, ldp, static_cast<int>(cp), V, ldv, static_cast<int>(w), d_coef,
                                             triangular ? 1 : 0, out, ldo, skip);
     };
     switch (wmax) {

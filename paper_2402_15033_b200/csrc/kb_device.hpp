@@ -6,9 +6,56 @@
 #include <cuda.h>
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+#include <utility>
+
 #include "kb_common.hpp"
 
+// First statement of every kernel: with programmatic dependent launch (below)
+// a kernel may start while its predecessor in the stream drains; it waits
+// here until that predecessor has completed and its writes are visible
+// (a no-op for a normally launched kernel).  Before any early return, so a
+// kernel never completes ahead of its predecessor.
+#define KB_PDL_WAIT() asm volatile("griddepcontrol.wait;" ::: "memory")
+
 namespace kb {
+
+// Kernel launch with programmatic dependent launch (PDL): the next kernel's
+// launch and CTA rasterisation overlap the previous kernel's tail.  Every
+// kernel of the library begins with KB_PDL_WAIT(), so stream order is kept.
+// KRY_PDL=0 launches normally (A/B).
+inline bool pdl_enabled() {
+    static const bool on = [] {
+        const char* e = std::getenv("KRY_PDL");
+        return !(e && std::atoi(e) == 0);
+    }();
+    return on;
+}
+inline cudaLaunchConfig_t pdl_config(dim3 grid, dim3 block, size_t smem, cudaStream_t s, cudaLaunchAttribute* at) {
+    cudaLaunchConfig_t cfg{};
+    cfg.gridDim = grid;
+    cfg.blockDim = block;
+    cfg.dynamicSmemBytes = smem;
+    cfg.stream = s;
+    at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+    at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+    cfg.attrs = at;
+    cfg.numAttrs = 1;
+    return cfg;
+}
+template <typename... KArgs, typename... Args>
+inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
+                       Args&&... args) {
+    cudaLaunchAttribute at[1];
+    const cudaLaunchConfig_t cfg = pdl_config(grid, block, smem, s, at);
+    KB_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
+}
+inline void launch_pdl_c(const void* kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, void** args) {
+    cudaLaunchAttribute at[1];
+    const cudaLaunchConfig_t cfg = pdl_config(grid, block, smem, s, at);
+    KB_CUDA(cudaLaunchKernelExC(&cfg, kernel, args));
+}
+
 namespace dev {
 
 __device__ __forceinline__ unsigned smem_u32(const void* p) {

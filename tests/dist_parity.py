@@ -89,6 +89,26 @@ def main():
         results[name] = {"bitwise": same}
         ok = ok and same
         del op
+    # Row-partitioned random-sparse CSR MPK: the segment-pipelined x gather
+    # (one broadcast per rank segment, slices aligned to the segments) keeps
+    # every row's stored summation order — bit-identical.
+    n = 6000
+    rng2 = np.random.default_rng(11)
+    cols = [np.unique(np.concatenate([[i], rng2.integers(0, n, 29)])) for i in range(n)]
+    rp_all = np.concatenate([[0], np.cumsum([len(c) for c in cols])]).astype(np.int64)
+    ci_all = np.concatenate(cols).astype(np.int64)
+    vv_all = rng2.uniform(-1.0, 1.0, ci_all.size)
+    a = ref.Csr(n, rp_all, ci_all, vv_all)
+    rb, re = rank * n // world, (rank + 1) * n // world
+    op = kb.CsrOperator(rp_all[rb:re + 1] - rp_all[rb], ci_all[rp_all[rb]:rp_all[re]],
+                        vv_all[rp_all[rb]:rp_all[re]], n_global=n, row_begin=rb, ctx=ctx)
+    start = rng.standard_normal(n)
+    want = ref.mpk(a, start, 5)[rb:re]
+    got = op.mpk(start[rb:re], 5)
+    same = bool(np.array_equal(got, want))
+    results["mpk_csr_random6000_s5"] = {"bitwise": same}
+    ok = ok and same
+    del op
     line = json.dumps({"rank": rank, "world": world, "ok": ok, "results": results})
     out_dir = os.environ.get("KRY_DIST_OUT")
     if out_dir:  # one file per rank (concurrent stdout lines can interleave)

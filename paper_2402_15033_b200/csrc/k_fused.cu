@@ -1,5 +1,7 @@
 // K6: the fused first-stage pass of the speculative two-stage path, 2-D
-// 5-point stencil, one rank.
+// 5-point stencil, one rank.  OPT-IN (KRY_FUSED_PASS=1): correct (every
+// two-stage 2-D golden passes through it) but slower than the separate
+// kernels on B200 — DESIGN.md §5 has the measurements.
 //
 // Between two first-stage blocks the unfused path streams the basis prefix
 // Q[:, 0:c0] twice: once in block j's update (K5t: Q_j = (V_j − P·R_col)·R_jj⁻¹)
@@ -7,35 +9,38 @@
 // block j+1's MPK (K2f) in between, because V_{j+1} = A^k·q (q = Q_j's last
 // column) needs the updated block.  For a stencil every row of V_{j+1} only
 // depends on rows of q within s grid lines / columns, so the three steps can
-// run in one pass over the rows: K6 updates a window of rows of block j,
-// feeds the new q into the s-level stencil wavefront and, s lines later,
-// accumulates the Gram of block j+1 over the same rows while they are still
-// in L2.  The prefix then crosses HBM once per block instead of twice.
+// run in one pass over the rows: K6 updates a window line of block j, feeds
+// the new q into the s-level stencil wavefront and, s lines later,
+// accumulates the Gram of block j+1 over the same rows.  The prefix then
+// crosses HBM once per block instead of twice.
 //
 // Work decomposition.  The grid is cut into 64-column windows (32 lanes ×
 // double2) that output their middle 64 − 2H columns (H = S rounded up to
-// even, as K2f), and the window-major (window, line) index space is split
-// into one contiguous range per CTA (1–3 window segments each).  A segment
-// [y0, y1) of window wx runs y1 − y0 + 2S line steps: the update computes
-// lines y0 − S … y1 + S − 1 (the 2S lines outside the segment and the H
-// halo columns are recomputed for the wavefront, never stored), level k of
-// the MPK trails the update by k lines, and the Gram takes line y0 + g at
-// step g + 2S.  Roles inside a CTA, synchronised by mbarrier rings:
-//   * kFuU update warps, one line per step round robin: update_acc (K5's
-//     arithmetic, term for term → bit-identical to K5/K5t), stores block j
-//     in place (core rows of the segment only), q into the next raw block,
-//     and q of all 64 columns into a shared ring for the MPK warp;
-//   * one MPK warp: the S-level skewed wavefront of K2f (same element order
-//     → bit-identical to S spmv calls), storing levels 1..S of the next raw
-//     block; signals the Gram when level S of a line is stored;
-//   * kFuG Gram warps, one line per step round robin: K3's DMMA tiles with
-//     rows as the MMA k dimension, fragments loaded from L2 (the rows were
-//     streamed or written ≤ 2S steps earlier), plus the panel-Gram pieces
-//     (NX extra tiles, kb_store.cpp).  Per-CTA partials in K3's packed tile
-//     layout, reduced by gram_reduce_kernel in a fixed order.
+// even, as K2f); tasks are (window, band) pairs in window-major order, task
+// i on CTA i mod grid, bands alternating direction (neighbouring windows
+// and band seams are processed at the same time, so the recomputed rows hit
+// L2).  A band [y0, y1) runs y1 − y0 + 2S line steps: the update computes
+// lines y0 − S … y1 + S − 1 (the 2S lines outside the band and the H halo
+// columns are recomputed for the wavefront, never stored), level k of the
+// MPK trails the update by k lines, the Gram takes the band's line g at step
+// g + 2S.  Roles, synchronised by mbarriers:
+//   * one TMA producer warp: window line l of [prefix | raw block j] into a
+//     ring slot (kBox rows per column);
+//   * kFuU update warps, line tt on warp tt mod kFuU: K5's arithmetic term
+//     for term (bit-identical to K5/K5t) from the slot; Q_j goes to the
+//     store (core rows), over the raw block in the slot (for the Gram), and
+//     q to the next raw block and to a shared ring for the MPK warp;
+//   * one MPK warp: levels 1..S of the wavefront, K2f's element order
+//     (bit-identical to S spmv calls), stored to the next raw block;
+//   * kFuG Gram warps, line g on warp g mod kFuG: K3's DMMA tiles from the
+//     slot (prefix and Q_j) and the stored levels, plus the panel-Gram pieces
+//     (NX extra tiles); per-CTA partials in K3's packed tile layout.
+//   A slot is freed after its line's Gram, S lines after its update, so the
+//   ring needs ≥ S + 2 slots (7 × 30 KB at c0 = 50) — the constraint that
+//   keeps the pass latency-bound.
 //
-// Races.  Windows overlap by 2H columns and segments recompute 2S lines, so
-// a CTA reads rows another CTA owns.  Both raw blocks therefore live outside
+// Races.  Windows overlap by 2H columns and bands recompute 2S lines, so a
+// CTA reads rows another CTA owns.  Both raw blocks therefore live outside
 // the store (Store::fraw_, double-buffered): the update reads raw block j
 // there and writes the store; the MPK writes raw block j+1 to the other
 // buffer.  The prefix Q[:, 0:c0] is read-only in the pass.

@@ -724,12 +724,10 @@ static int solve_common(kry_ctx* ctx, kry_operator* op, const double* b, const d
         if (device) {
             rep = kb::gmres(c, *op->op, b, x0, *cfg, standard, x_out, &ctx->ws);
         } else {
-            const i64 ld = kb::device_ld(n);
             double* db = upload(c, ctx->up0, b, n, 1);
             double* dx0 = x0 ? upload(c, ctx->up1, x0, n, 1) : nullptr;
-            ctx->up2.ensure(static_cast<size_t>(ld) * 8);
-            rep = kb::gmres(c, *op->op, db, dx0, *cfg, standard, ctx->up2.p, &ctx->ws);
-            download(c, x_out, ctx->up2.p, ld, n, 1);
+            // the solution streams to x_out while the last update is computed
+            rep = kb::gmres(c, *op->op, db, dx0, *cfg, standard, nullptr, &ctx->ws, x_out);
             c.sync();
         }
         fill_report(rep, report);

@@ -30,8 +30,15 @@ struct Vec {
 
 }  // namespace
 
+Workspace::~Workspace() {
+    for (cudaEvent_t e : chunk_ev)
+        if (e) cudaEventDestroy(e);
+    if (copy_done) cudaEventDestroy(copy_done);
+    if (copy_stream) cudaStreamDestroy(copy_stream);
+}
+
 Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, const kry_solver_config& cfg_in,
-             bool standard_mode, double* d_x_out, Workspace* ws) {
+             bool standard_mode, double* d_x_out, Workspace* ws, double* h_x_out) {
     kry_solver_config cfg = cfg_in;
     if (standard_mode) {  // standard_gmres (gmres.hpp:404-411)
         cfg.step = 1;
@@ -83,9 +90,24 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
     double r_norm = residual(x.p, r.p);
     const double r0 = r_norm;
     rep.initial_residual = r0;
+    // Host output: h_x_out holds x once copy_done has fired, when host_x_ok.
+    bool host_x_ok = false;
+    if (h_x_out && !W.copy_stream) {
+        KB_CUDA(cudaStreamCreateWithFlags(&W.copy_stream, cudaStreamNonBlocking));
+        for (cudaEvent_t& e : W.chunk_ev) KB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+        KB_CUDA(cudaEventCreateWithFlags(&W.copy_done, cudaEventDisableTiming));
+    }
     auto finish = [&]() {
         if (d_x_out)
             KB_CUDA(cudaMemcpyAsync(d_x_out, x.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, ctx.stream));
+        if (h_x_out) {
+            if (host_x_ok) {
+                KB_CUDA(cudaStreamWaitEvent(ctx.stream, W.copy_done, 0));
+            } else {  // no (accepted) update streamed out: download x now
+                KB_CUDA(cudaStreamWaitEvent(ctx.stream, W.copy_done, 0));  // (an in-flight copy of a rejected update)
+                KB_CUDA(cudaMemcpyAsync(h_x_out, x.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToHost, ctx.stream));
+            }
+        }
         ctx.sync();
         ctx.resolve_timers();
         rep.wall_seconds =
@@ -150,16 +172,32 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         if (!res.implicit_crossed && !force) return res;
 
         cudaEvent_t t0 = ctx.begin_phase();
-        const double* src = x.p;
-        if (lsq.valid_cols == 0)
-            KB_CUDA(cudaMemcpyAsync(xn.p, x.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, ctx.stream));
-        for (i64 l0 = 0; l0 < lsq.valid_cols; l0 += 64) {
-            Coef64 y{};
-            const int cnt = static_cast<int>(std::min<i64>(64, lsq.valid_cols - l0));
-            for (int i = 0; i < cnt; ++i) y.v[i] = ycoef[l0 + i];
-            launch_xupdate(ctx.stream, n, src, store.col(l0), store.ld(), cnt, y, xn.p, ctx.launches);
-            src = xn.p;
+        // x_new = x + Q·y in row chunks; with a host output each chunk is
+        // copied out on the side stream as soon as it is written
+        const int nchunk = h_x_out ? 4 : 1;
+        if (h_x_out) KB_CUDA(cudaStreamWaitEvent(ctx.stream, W.copy_done, 0));  // xn may still be going out
+        for (int ch = 0; ch < nchunk; ++ch) {
+            const i64 r0c = n * ch / nchunk, r1c = n * (ch + 1) / nchunk;
+            const double* src = x.p + r0c;
+            if (lsq.valid_cols == 0)
+                KB_CUDA(cudaMemcpyAsync(xn.p + r0c, src, static_cast<size_t>(r1c - r0c) * 8, cudaMemcpyDeviceToDevice,
+                                        ctx.stream));
+            for (i64 l0 = 0; l0 < lsq.valid_cols; l0 += 64) {
+                Coef64 y{};
+                const int cnt = static_cast<int>(std::min<i64>(64, lsq.valid_cols - l0));
+                for (int i = 0; i < cnt; ++i) y.v[i] = ycoef[l0 + i];
+                launch_xupdate(ctx.stream, r1c - r0c, src, store.col(l0) + r0c, store.ld(), cnt, y, xn.p + r0c,
+                               ctx.launches);
+                src = xn.p + r0c;
+            }
+            if (h_x_out && r1c > r0c) {
+                KB_CUDA(cudaEventRecord(W.chunk_ev[ch], ctx.stream));
+                KB_CUDA(cudaStreamWaitEvent(W.copy_stream, W.chunk_ev[ch], 0));
+                KB_CUDA(cudaMemcpyAsync(h_x_out + r0c, xn.p + r0c, static_cast<size_t>(r1c - r0c) * 8,
+                                        cudaMemcpyDeviceToHost, W.copy_stream));
+            }
         }
+        if (h_x_out) KB_CUDA(cudaEventRecord(W.copy_done, W.copy_stream));
         rep.mpk_bytes += 0;  // the residual's SpMV is restart-loop traffic
         ctx.end_phase(PH_RESTART, t0);
         const double rnv = residual(xn.p, rn.p);
@@ -169,6 +207,9 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
             std::swap(r.p, rn.p);
             r_norm = rnv;
             res.applied = true;
+            host_x_ok = h_x_out != nullptr;  // the copy going out is x
+        } else {
+            host_x_ok = false;  // the host got the rejected update
         }
         return res;
     };

@@ -36,11 +36,23 @@ struct Workspace {
     i64 n = -1, m = -1, s = -1, shat = -1;
     std::unique_ptr<Store> store;
     DevBuf x, xn, r, rn;
+    // host-output path: the solution update streams to the host while it is
+    // computed (side stream, one event per row chunk)
+    cudaStream_t copy_stream = nullptr;
+    cudaEvent_t chunk_ev[4] = {}, copy_done = nullptr;
+    Workspace() = default;
+    Workspace(const Workspace&) = delete;
+    Workspace& operator=(const Workspace&) = delete;
+    ~Workspace();
 };
 
-// d_b: n_local rhs (device); d_x0 may be null (or alias d_x_out); d_x_out may be null.
+// d_b: n_local rhs (device); d_x0 may be null (or alias d_x_out); d_x_out may
+// be null.  h_x_out (host; pinned for the overlap to happen) receives the
+// solution instead of d_x_out: every applied solution update is copied to
+// it chunk by chunk as the update kernel produces it, so the final download
+// overlaps the update and the acceptance check (re-downloaded if rejected).
 Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, const kry_solver_config& cfg,
-             bool standard_mode, double* d_x_out, Workspace* ws = nullptr);
+             bool standard_mode, double* d_x_out, Workspace* ws = nullptr, double* h_x_out = nullptr);
 
 void validate_config(const kry_solver_config& cfg);
 

@@ -676,10 +676,12 @@ void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const 
     auto go = [&](auto kernel) {
         // One wave of resident warps, one (window, band) task each: bands as
         // tall as that allows (the 2s-line band overlap is recomputed), at
-        // least 2s lines; very wide grids loop over tasks.
+        // least 2 lines; very wide grids loop over tasks.  A warp walks
+        // band + 2s − 1 dependent steps, so on small grids (idle warps) short
+        // bands win: 512², s = 5: 16.9 → ~10 µs per block with 2-line bands.
         const int per_sm = occupancy(reinterpret_cast<const void*>(kernel), kBlock, 0);
         const i64 resident = static_cast<i64>(num_sms()) * std::max(per_sm, 1) * (kBlock / 32);
-        const i64 nbands = std::max<i64>(1, std::min<i64>(resident / nwx, g.lines / (2 * s)));
+        const i64 nbands = std::max<i64>(1, std::min<i64>(resident / nwx, g.lines / 2));
         const i64 band = ceil_div(g.lines, nbands);
         const i64 ntasks = nwx * ceil_div(g.lines, band);
         const unsigned grid = static_cast<unsigned>(

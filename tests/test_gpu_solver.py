@@ -160,6 +160,31 @@ def test_repeat_solves_are_deterministic(kb, ctx):
     np.testing.assert_array_equal(r1.solution, r2.solution)
 
 
+@pytest.mark.parametrize("grid,kind,shat,max_iters,x0", [(96, 3, 60, 500000, None), (200, 2, 0, 120, None),
+                                                          (150, 3, 30, 180, 0.5), (64, 3, 60, 500000, 1.0)])
+def test_host_output_stream_matches_device_path(kb, ctx, grid, kind, shat, max_iters, x0):
+    """The host-buffer entry point streams the solution out in row chunks
+    while the update runs (kb_gmres.cpp, side stream, re-download when an
+    update is rejected): the same report and the same solution bits as the
+    device-resident entry point."""
+    import torch
+
+    op = kb.Laplace2D(grid, grid)
+    b = op.spmv(np.ones(op.n))
+    x0v = None if x0 is None else np.full(op.n, x0)
+    cfg = kb.SolverConfig(scheme=kb.OrthoScheme(kb.OrthoKind(kind), shat), big_step=shat, max_iters=max_iters)
+    host = kb.sstep_gmres(op, b, x0v, cfg)
+    db = torch.from_numpy(b).cuda()
+    dx0 = None if x0v is None else torch.from_numpy(x0v).cuda()
+    dx = torch.empty(op.n, dtype=torch.float64, device="cuda")
+    torch.cuda.synchronize()  # the library runs on its own stream
+    dev = kb.sstep_gmres_device(op, db.data_ptr(), None if dx0 is None else dx0.data_ptr(), cfg, dx.data_ptr())
+    assert (host.status, host.iterations, host.restarts, host.sync.reduces) == (
+        dev.status, dev.iterations, dev.restarts, dev.sync.reduces)
+    assert host.cycle_residuals == dev.cycle_residuals
+    np.testing.assert_array_equal(host.solution, dx.cpu().numpy())
+
+
 def test_config_validation(kb, ctx):
     op = kb.Laplace2D(8, 8)
     b = np.ones(64)

@@ -87,8 +87,10 @@ double* Store::scratch(int which, i64 w) {
 
 bool Store::can_speculate(i64 w) const {
     // one prefix group (round_up(c0,8) + 8 ≤ 64) for every block of the
-    // cycle, and the fused panel-Gram bookkeeping this path assumes
-    return w >= 1 && w <= 8 && max_cols_ <= 64 && fused_panel_gram_;
+    // cycle — the last block's prefix is c0 = capacity − w (s = 1..4 with
+    // m = 60 exceed it: c0 = 59 at w = 2) — and the fused panel-Gram
+    // bookkeeping this path assumes
+    return w >= 1 && w <= 8 && round_up(max_cols_ - w, 8) + 8 <= 64 && fused_panel_gram_;
 }
 
 bool Store::spec_panel_full() const {

@@ -1,6 +1,7 @@
 """Randomised solver parity sweep against the live reference (oracle/_ref):
 random sparse / stencil operators, restart lengths, step sizes, schemes.
-Prints one line per case and a summary; exit code = number of mismatches."""
+Prints one line per case and a summary; exit code = number of mismatches.
+usage: python tools/fuzz_parity.py SEED NCASES [wide]   (wide: m ≤ 128, s ≤ 8)"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -10,11 +11,13 @@ from oracle import ref
 FMA = ref._load(os.path.join(os.path.dirname(ref.__file__), "_ref", "libkrylov_ref_fma.so"))
 rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 ncases = int(sys.argv[2]) if len(sys.argv) > 2 else 40
+wide = len(sys.argv) > 3 and sys.argv[3] == "wide"  # m up to 128, s up to 8
 bad = 0
+skipped = 0
 for case in range(ncases):
     kind = int(rng.choice([1, 2, 3, 3]))
-    s = int(rng.integers(1, 8))
-    m = s * int(rng.integers(2, max(3, 61 // s)))
+    s = int(rng.integers(1, 9 if wide else 8))
+    m = s * int(rng.integers(2, max(3, (129 if wide else 61) // s)))
     shat = 0 if kind != 3 else s * int(rng.integers(1, m // s + 1))
     opk = rng.choice(["lap2d", "lap3d", "rand"])
     if opk == "lap2d":
@@ -75,8 +78,12 @@ for case in range(ncases):
             msg += f" got {(int(got.status), got.iterations, got.restarts, got.sync.reduces)} want {(want.status, want.iterations, want.restarts, want.reduces)}"
     except Exception as e:  # noqa: BLE001
         ok, msg = False, f"EXC {type(e).__name__}: {e}"
-    bad += 0 if ok else 1
+        if "above 64 columns" in str(e):  # documented device-path limit: ŝ+1 ≤ 64
+            ok, msg = None, "documented limit (block width above 64 columns)"
+    bad += 1 if ok is False else 0
+    skipped += 1 if ok is None else 0
+    tag = "ok " if ok else ("SKIP" if ok is None else "BAD")
     print(f"case {case:3d} {opk:5s} n={a.n:6d} kind={kind} m={m:3d} s={s} shat={shat:3d} its<={max_iters:4d}: "
-          f"{'ok ' if ok else 'BAD'} {msg}", flush=True)
-print(f"{ncases - bad}/{ncases} ok")
+          f"{tag} {msg}", flush=True)
+print(f"{ncases - bad - skipped}/{ncases - skipped} ok" + (f" ({skipped} at the documented width limit)" if skipped else ""))
 sys.exit(bad)

@@ -24,6 +24,29 @@ std::vector<std::pair<i64, i64>> groups_for(i64 c0, i64 w) {
 void gram_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
                  Mat& r_col, Mat& g, i64 x_first, i64 x_count, Mat* gx) {
     dim_check(w >= 1, "gram of empty matrix");
+    if (round_up(w, 8) > 64) {
+        // V wider than one 64-slot pass (a finalize panel ŝ + 1 > 64, e.g.
+        // m = 120, ŝ = 120): V = [V1 V2], V1 64 columns — PᵀV1 and V1ᵀV1,
+        // then V1ᵀV2 and V2ᵀV2 (V1 as the prefix), then PᵀV2 (recursive in V2).
+        const i64 w1 = 64, w2 = w - w1;
+        const double* V2 = V + w1 * ldv;
+        Mat rc1, g11, r12, g22, rc2, gtmp;
+        gram_device(ctx, n, P, ldp, c0, V, ldv, w1, rc1, g11);
+        gram_device(ctx, n, V, ldv, w1, V2, ldv, w2, r12, g22);
+        if (c0 > 0) gram_device(ctx, n, P, ldp, c0, V2, ldv, w2, rc2, gtmp);
+        r_col = Mat(c0, w);
+        g = Mat(w, w);
+        for (i64 j = 0; j < w; ++j)
+            for (i64 l = 0; l < c0; ++l) r_col(l, j) = j < w1 ? rc1(l, j) : rc2(l, j - w1);
+        for (i64 j = 0; j < w1; ++j)
+            for (i64 i = 0; i < w1; ++i) g(i, j) = g11(i, j);
+        for (i64 j = 0; j < w2; ++j) {
+            for (i64 i = 0; i < w1; ++i) g(i, w1 + j) = g(w1 + j, i) = r12(i, j);
+            for (i64 i = 0; i < w2; ++i) g(w1 + i, w1 + j) = g22(i, j);
+        }
+        if (gx) *gx = Mat();
+        return;
+    }
     // Launch plan: one pass per (V column range, prefix group).  A Gram pass
     // holds at most 64 column slots, so a prefix is split into groups that
     // fit beside V; a V wider than 56 columns with a prefix (a finalize of
@@ -122,8 +145,40 @@ void update_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const doub
     if (triangular)
         for (i64 j = 0; j < w; ++j)
             if (r_jj(j, j) == 0.0) fail(KRY_SINGULAR_FACTOR, "triangular factor has a zero diagonal entry");
-    if (round_up(w, 8) > 64)
-        fail(KRY_UNSUPPORTED, "block width above 64 columns is not supported on the device path");
+    if (round_up(w, 8) > 64) {
+        // Blocked: Q1 = (V1 − P·R_col1)·R11⁻¹; then V2 − P·R_col2 (stored),
+        // and that minus Q1·R12, times R22⁻¹ (Q1 as the prefix).  On the
+        // substitution kernels every element receives its terms in the
+        // unblocked order (prefix, block-1 columns, block-2 columns, then
+        // ×1/r_jj) — one wide substitution, term for term.
+        const i64 w1 = 64, w2 = w - w1;
+        Mat rc1(c0, w1), rc2(c0, w2), r12(w1, w2);
+        Upper r11(w1), r22(w2), none(w2);
+        for (i64 l = 0; l < c0; ++l) {
+            for (i64 j = 0; j < w1; ++j) rc1(l, j) = r_col(l, j);
+            for (i64 j = 0; j < w2; ++j) rc2(l, j) = r_col(l, w1 + j);
+        }
+        for (i64 j = 0; j < w1; ++j)
+            for (i64 i = 0; i <= j; ++i) r11.at(i, j) = r_jj(i, j);
+        for (i64 j = 0; j < w2; ++j) {
+            for (i64 i = 0; i < w1; ++i) r12(i, j) = r_jj(i, w1 + j);
+            for (i64 i = 0; i <= j; ++i) r22.at(i, j) = r_jj(w1 + i, w1 + j);
+        }
+        const double* V2 = V + w1 * ldv;
+        double* out2 = out + w1 * ldo;
+        // (each call stages its coefficients through ctx.h_coef / ctx.coef:
+        // wait for the previous launch before the next one reuses them)
+        update_device(ctx, n, P, ldp, c0, V, ldv, w1, rc1, r11, out, ldo, triangular);
+        ctx.sync();
+        if (c0 > 0) {
+            update_device(ctx, n, P, ldp, c0, V2, ldv, w2, rc2, none, out2, ldo, /*triangular=*/false);
+            ctx.sync();
+        } else if (out2 != V2) {
+            KB_CUDA(cudaMemcpy2DAsync(out2, ldo * 8, V2, ldv * 8, n * 8, w2, cudaMemcpyDeviceToDevice, ctx.stream));
+        }
+        if (triangular) update_device(ctx, n, out, ldo, w1, out2, ldo, w2, r12, r22, out2, ldo, true);
+        return;
+    }
     if (triangular && w >= 17 && round_up(w, 8) + round_up(c0, 8) <= 64) {
         // Wide, well-conditioned R_jj (finalize / second pass): substitution
         // as a DMMA GEMM against the explicit inverse (k_tsqr.cu, K5b).

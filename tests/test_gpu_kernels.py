@@ -180,6 +180,25 @@ def test_bcgs_pip_matches_reference(kb, ctx, ref, rng, n, c0, w):
     assert np.all(np.diag(res.r_jj) > 0)
 
 
+@pytest.mark.parametrize("n,c0,w", [(3000, 0, 70), (3000, 0, 81), (3000, 12, 75), (2000, 40, 129)])
+def test_wide_blocks_match_reference(kb, ctx, ref, rng, n, c0, w):
+    """Blocks wider than one 64-slot pass (finalize panels ŝ + 1 > 64):
+    blocked Gram and blocked substitution (kb_ortho.cpp)."""
+    q = orthonormal(rng, n, c0) if c0 else None
+    v = rng.standard_normal((n, w))
+    rc, g = kb.gram(q, v)
+    assert rel(g, ref.gram(v)) < 1e-13
+    if c0:
+        assert rel(rc, ref.mat_mul_tn(q, v)) < 1e-13
+    sync = kb.SyncCounter()
+    res = kb.bcgs_pip(q, v, sync)
+    q_ref, rc_ref, rj_ref, red = ref.bcgs_pip(q, v)
+    assert rel(res.r_jj, rj_ref) < 1e-12
+    assert rel(res.q, q_ref) < 1e-11
+    if c0:
+        assert rel(res.r_col, rc_ref) < 1e-12
+
+
 def test_bcgs_pip_empty_prefix_is_cholqr(kb, ctx, rng):
     # BcgsPip.EmptyPrefixIsCholQrBitwise (tests/test_block_ortho.cpp:172-181)
     v = rng.standard_normal((120, 5))

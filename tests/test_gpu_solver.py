@@ -225,13 +225,15 @@ def test_random_sparse_csr_parity(kb, ctx, ref, kind, shat):
 
 
 @pytest.mark.parametrize("m,s,shat,kind", [(120, 5, 60, 3), (120, 5, 0, 2), (40, 4, 20, 3), (30, 6, 30, 3),
-                                           (60, 1, 24, 3), (60, 2, 30, 3), (60, 4, 60, 3), (56, 7, 56, 3)])
+                                           (60, 1, 24, 3), (60, 2, 30, 3), (60, 4, 60, 3), (56, 7, 56, 3),
+                                           (120, 5, 120, 3), (100, 4, 80, 3)])
 def test_other_restart_lengths_match_live_reference(kb, ctx, ref, m, s, shat, kind):
     """Restart lengths / step sizes off the default: m = 120 (prefix groups
     beyond one 64-slot Gram, no speculation, two big panels), s = 1, 2, 4,
     6, 7 (the last blocks' prefixes at m = 60 need a second 64-slot group
-    for s ≤ 4: the synchronous path) — same counts as the live reference and
-    cycle 1 within 1e-10."""
+    for s ≤ 4: the synchronous path), finalize panels wider than 64 columns
+    (ŝ = 120, 80: blocked Gram and substitution) — same counts as the live
+    reference and cycle 1 within the protocol."""
     grid = 48
     a = ref.laplace2d(grid, grid)
     b = ref.spmv(a, np.ones(a.n))

@@ -87,28 +87,40 @@ __global__ void __launch_bounds__(kPipThreads) pip_block_kernel(const PipBlockAr
         if (i > j) s[i + j * kPipMaxW] = s[j + i * kPipMaxW];
     }
     __syncthreads();
-    // 3. try_cholesky (dense_kernels.hpp:111-127) on one thread, exact order.
-    if (tid == 0) {
+    // 3. try_cholesky (dense_kernels.hpp:111-127), row by row on one warp.
+    //    Every entry keeps the reference's exact operation sequence
+    //    (r_ij = (s_ij − Σ_{k<i} r_ki·r_kj in k order) / r_ii, the diagonal
+    //    likewise then sqrt), so the factor is bit-identical; only independent
+    //    entries run concurrently: the critical path is w sqrt + w divisions
+    //    instead of w sqrt + w(w−1)/2 divisions.  The first non-positive
+    //    diagonal is the reference's pivot (row i's diagonal needs exactly the
+    //    columns < i the reference has finished when it reaches column i).
+    if (tid < 32) {
         int piv = 0;
         if (a.prev_slot && a.prev_slot[kSlotStatus] != 0.0) piv = -1;  // an earlier block failed
-        for (int j = 0; j < w && piv == 0; ++j) {
-            for (int i = 0; i < j; ++i) {
+        for (int i = 0; i < w && piv == 0; ++i) {
+            double d = s[i + i * kPipMaxW];  // every lane: same value, no broadcast
+            for (int k = 0; k < i; ++k) d = __dsub_rn(d, __dmul_rn(r[k + i * kPipMaxW], r[k + i * kPipMaxW]));
+            if (!(d > 0.0)) {
+                piv = i + 1;
+                break;
+            }
+            const double rii = __dsqrt_rn(d);
+            const int j = tid;
+            if (j == i) r[i + i * kPipMaxW] = rii;
+            if (j > i && j < w) {
                 double acc = s[i + j * kPipMaxW];
                 for (int k = 0; k < i; ++k)
                     acc = __dsub_rn(acc, __dmul_rn(r[k + i * kPipMaxW], r[k + j * kPipMaxW]));
-                r[i + j * kPipMaxW] = __ddiv_rn(acc, r[i + i * kPipMaxW]);
+                r[i + j * kPipMaxW] = __ddiv_rn(acc, rii);
             }
-            double d = s[j + j * kPipMaxW];
-            for (int k = 0; k < j; ++k) d = __dsub_rn(d, __dmul_rn(r[k + j * kPipMaxW], r[k + j * kPipMaxW]));
-            if (!(d > 0.0)) {
-                piv = j + 1;
-                break;
-            }
-            r[j + j * kPipMaxW] = __dsqrt_rn(d);
+            __syncwarp();
         }
-        bad = piv;
-        a.slot[kSlotStatus] = static_cast<double>(piv);
-        *a.skip = piv != 0 ? 1 : 0;
+        if (tid == 0) {
+            bad = piv;
+            a.slot[kSlotStatus] = static_cast<double>(piv);
+            *a.skip = piv != 0 ? 1 : 0;
+        }
     }
     __syncthreads();
     // 4. result slot (host replay) and the K5 coefficients

@@ -379,8 +379,11 @@ __device__ __forceinline__ void mpk2d_task(const StencilGeom& g, const double* _
 #pragma unroll
     for (int q = 0; q < kMpkRing; ++q) pf[q] = load(ls + q);
     double* const out_ix = out + ix;
-    auto step = [&](auto phase, int st) {
+    // FAST: every level's line this step lies inside the band and the grid
+    // (warp-uniform), so the per-level line checks drop out; same values.
+    auto step = [&](auto phase, auto fast, int st) {
         constexpr int P = decltype(phase)::value;  // st ≡ P (mod 3)
+        constexpr bool FAST = decltype(fast)::value;
         constexpr int P1 = (P + 2) % 3, P2 = (P + 1) % 3, P3 = P;  // steps t−1, t−2, t−3
         const int L = ls + st;
         const double2 in = pf[P];
@@ -408,18 +411,26 @@ __device__ __forceinline__ void mpk2d_task(const StencilGeom& g, const double* _
             s1 = __dadd_rn(s1, -right);
             s1 = __dadd_rn(s1, -up.y);
             // outside the grid (lines or columns): exactly +0.0
-            const bool live = in_grid && gl >= 0 && gl < ny;
+            const bool live = in_grid && (FAST || (gl >= 0 && gl < ny));
             const double2 v = live ? make_double2(s0, s1) : make_double2(0.0, 0.0);
-            if (store_lane && l >= y0 && l < y1)
+            if (store_lane && (FAST || (l >= y0 && l < y1)))
                 *reinterpret_cast<double2*>(orow + ((k - 1) * ldo - (2 * k - 1) * nx64)) = v;
             if (k < S) r[P][k] = v;
         }
         r[P][0] = in;
     };
+    const int lo_ok = max(y0, -line0), hi_ok = min(y1, ny - line0);
     for (int st = 0; st < steps; st += kMpkRing) {  // steps past the end are harmless (nothing stored)
-        step(std::integral_constant<int, 0>{}, st);
-        step(std::integral_constant<int, 1>{}, st + 1);
-        step(std::integral_constant<int, 2>{}, st + 2);
+        // levels' lines over these three steps: ls + st − 2S + 1 … ls + st + 1
+        if (ls + st - 2 * S + 1 >= lo_ok && ls + st + 1 < hi_ok) {
+            step(std::integral_constant<int, 0>{}, std::true_type{}, st);
+            step(std::integral_constant<int, 1>{}, std::true_type{}, st + 1);
+            step(std::integral_constant<int, 2>{}, std::true_type{}, st + 2);
+        } else {
+            step(std::integral_constant<int, 0>{}, std::false_type{}, st);
+            step(std::integral_constant<int, 1>{}, std::false_type{}, st + 1);
+            step(std::integral_constant<int, 2>{}, std::false_type{}, st + 2);
+        }
     }
 }
 

@@ -20,6 +20,7 @@
 // DeviceError (there is no CPU fallback).
 #pragma once
 
+#include <algorithm>
 #include <cmath>
 #include <cstring>
 #include <memory>
@@ -458,18 +459,37 @@ inline SolveReport solve(bool standard, const Operator& a, std::span<const doubl
     if (!x0.empty() && x0.size() != n) throw DimensionMismatch("x0 length");
     SolveReport rep;
     rep.solution.assign(n, 0.0);
-    std::vector<double> cyc(1 << 16);
-    std::vector<int64_t> pb(1 << 18), pbp(1 << 16);
+    // The reference's SolveReport keeps every entry: size the history
+    // buffers from max_iters (one per-block entry per s iterations, at most
+    // one cycle per s iterations) and, should a run still report more
+    // entries than fit, re-run with buffers of the reported size.
+    const int64_t step = standard ? 1 : std::max<int64_t>(1, static_cast<int64_t>(cfg.step));
+    const int64_t iters = static_cast<int64_t>(std::min<index_t>(cfg.max_iters, index_t(1) << 40));
+    int64_t cap_c = std::min<int64_t>(iters / step + 64, int64_t(1) << 24);
+    int64_t cap_b = std::min<int64_t>(2 * (iters / step) + 64, int64_t(1) << 25);
+    std::vector<double> cyc;
+    std::vector<int64_t> pb, pbp;
     kry_report r{};
-    r.cycle_residuals = cyc.data();
-    r.cycle_residuals_cap = static_cast<int64_t>(cyc.size());
-    r.per_block = pb.data();
-    r.per_block_cap = static_cast<int64_t>(pb.size());
-    r.per_big_panel = pbp.data();
-    r.per_big_panel_cap = static_cast<int64_t>(pbp.size());
     const kry_solver_config c = cfg.to_c();
     auto fn = standard ? kry_standard_gmres : kry_sstep_gmres;
-    check(fn(a.context().get(), a.get(), b.data(), x0.empty() ? nullptr : x0.data(), &c, &r, rep.solution.data()));
+    for (int attempt = 0;; ++attempt) {
+        cyc.assign(static_cast<size_t>(cap_c), 0.0);
+        pb.assign(static_cast<size_t>(cap_b), 0);
+        pbp.assign(static_cast<size_t>(cap_c), 0);
+        r = kry_report{};
+        r.cycle_residuals = cyc.data();
+        r.cycle_residuals_cap = cap_c;
+        r.per_block = pb.data();
+        r.per_block_cap = cap_b;
+        r.per_big_panel = pbp.data();
+        r.per_big_panel_cap = cap_c;
+        check(fn(a.context().get(), a.get(), b.data(), x0.empty() ? nullptr : x0.data(), &c, &r,
+                 rep.solution.data()));
+        if ((r.n_cycle_residuals <= cap_c && r.n_per_block <= cap_b && r.n_per_big_panel <= cap_c) || attempt > 0)
+            break;
+        cap_c = std::max({cap_c, r.n_cycle_residuals, r.n_per_big_panel});
+        cap_b = std::max(cap_b, r.n_per_block);
+    }
     rep.status = static_cast<SolveStatus>(r.status);
     rep.iterations = static_cast<index_t>(r.iterations);
     rep.restarts = static_cast<index_t>(r.restarts);

@@ -218,8 +218,17 @@ def _p(a: Optional[np.ndarray]):
     return None if a is None else a.ctypes.data_as(P_dbl)
 
 
+def _report_cap(cfg: "SolverConfig", standard: bool = False) -> int:
+    """History entries a solve can produce: one per-block entry per s
+    iterations (plus truncation retries), at most one cycle per s iterations."""
+    step = 1 if standard else max(1, cfg.step)
+    return 2 * (min(cfg.max_iters, 1 << 40) // step) + 64
+
+
 def _report_from_c(rep: kry_report, cyc, pb, pbp, solution) -> SolveReport:
     n1, n2, n3 = rep.n_cycle_residuals, rep.n_per_block, rep.n_per_big_panel
+    if n1 > len(cyc) or n2 > len(pb) or n3 > len(pbp):  # never truncate the history silently
+        raise KrylovError(f"report history overflow ({n1}/{n2}/{n3} entries, capacity {len(cyc)})")
     tel = {k: getattr(rep, k) for k in (
         "mpk_seconds", "ortho_seconds", "gram_kernel_seconds", "update_kernel_seconds",
         "restart_seconds", "mpk_bytes", "ortho_bytes", "gram_bytes", "update_bytes",
@@ -641,7 +650,7 @@ def _solve(fn, op: Operator, b, x0, cfg: SolverConfig, want_solution=True) -> So
         if x0a.shape != (op.n,):
             raise DimensionMismatch("dimension mismatch: x0 length")
     x = np.zeros(op.n) if want_solution else None
-    rep, cyc, pb, pbp = _new_report()
+    rep, cyc, pb, pbp = _new_report(_report_cap(cfg, fn == lib().kry_standard_gmres))
     c = cfg.to_c()
     _check(fn(op.ctx.handle, op.handle, _p(b), _p(x0a), C.byref(c), C.byref(rep), _p(x)))
     return _report_from_c(rep, cyc, pb, pbp, x)
@@ -659,7 +668,7 @@ def standard_gmres(op: Operator, b, x0, cfg: SolverConfig) -> SolveReport:
 
 def _solve_device(fn, op: Operator, d_b: int, d_x0: Optional[int], cfg: SolverConfig,
                   d_x_out: Optional[int]) -> SolveReport:
-    rep, cyc, pb, pbp = _new_report()
+    rep, cyc, pb, pbp = _new_report(_report_cap(cfg, fn == lib().kry_standard_gmres_device))
     c = cfg.to_c()
     _check(fn(op.ctx.handle, op.handle, C.c_void_p(d_b), C.c_void_p(d_x0) if d_x0 else None, C.byref(c),
               C.byref(rep), C.c_void_p(d_x_out) if d_x_out else None))

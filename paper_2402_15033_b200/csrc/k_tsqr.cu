@@ -748,6 +748,10 @@ size_t gram_stage_bytes() {
 }
 
 TsParams geometry(i64 n, int w, int cp, bool gram) {
+    // TMA tile coordinates are signed 32-bit (cp.async.bulk.tensor): the row
+    // of every tile must be < 2^31.  (2^31 rows × 61 columns would be a 1 TB
+    // store, far beyond one GPU, but the limit is checked, not assumed.)
+    if (n >= (i64(1) << 31)) fail(KRY_UNSUPPORTED, "more than 2^31 - 1 rows per GPU on the TMA Gram/update path");
     TsParams p{};
     p.n = n;
     p.w = w;

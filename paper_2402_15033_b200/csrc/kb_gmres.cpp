@@ -97,6 +97,15 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         for (cudaEvent_t& e : W.chunk_ev) KB_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
         KB_CUDA(cudaEventCreateWithFlags(&W.copy_done, cudaEventDisableTiming));
     }
+    // Every exit (including an exception from SingularR, NCCL or CUDA) waits
+    // for the chunked solution copies: the ABI must not return while DMA is
+    // still writing the caller's buffer.
+    struct CopyGuard {
+        cudaStream_t s;
+        ~CopyGuard() {
+            if (s) cudaStreamSynchronize(s);
+        }
+    } copy_guard{h_x_out ? W.copy_stream : nullptr};
     auto finish = [&]() {
         if (d_x_out)
             KB_CUDA(cudaMemcpyAsync(d_x_out, x.p, static_cast<size_t>(n) * 8, cudaMemcpyDeviceToDevice, ctx.stream));

@@ -237,8 +237,15 @@ bool Operator::mpk(const double* x, double* out, i64 ldo, int s) {
     Ctx& c = *ctx;
     // Every rank must own at least s lines (the halo is the neighbour's s
     // edge lines); the partition differs by at most one line between ranks.
-    if (mode == 0 || kind != LAPLACE2D || geom.ny / c.nranks < s ||
-        !mpk2d_supported(geom, s, x, out, ldo, mode == 2))
+    // The choice pairs every rank's sends with its neighbours' receives, so
+    // it must be the same on every rank: the size heuristic is judged on the
+    // smallest rank's line count (ny / nranks, known to all ranks), not on
+    // this rank's own.  The other inputs (s, nx, the store's even ld, 256-byte
+    // aligned allocations) are identical on every rank.
+    StencilGeom uniform = geom;
+    uniform.lines = geom.ny / c.nranks;
+    if (mode == 0 || kind != LAPLACE2D || uniform.lines < s ||
+        !mpk2d_supported(uniform, s, x, out, ldo, mode == 2))
         return false;
     const i64 h = static_cast<i64>(s) * geom.nx;
     if (c.nranks > 1) {

@@ -466,16 +466,20 @@ Store::OrthoRes Store::run_scheme(i64 c0, const double* V, i64 ldv, i64 w, int k
             double* s0 = scratch(0, w);
             double* s1 = scratch(1, w);
             // intra: CholQR (single column) or CholQR2; input x → output dst.
-            auto intra = [&](const double* x, i64 ldx, double* dst) -> Upper {
+            // The first CholQR of CholQR2 writes `mid`, only the second writes
+            // dst: V may alias dst (the solver feeds blocks in place), and a
+            // failure of the second pass must leave V raw for the retry and
+            // record_seam (append_impl, basis_store.hpp:169-209).
+            auto intra = [&](const double* x, i64 ldx, double* mid, double* dst) -> Upper {
                 if (single) return cholqr_device(ctx_, n_, x, ldx, w, dst, ld_, sync, ortho_bytes);
-                Upper r1 = cholqr_device(ctx_, n_, x, ldx, w, dst, ld_, sync, ortho_bytes);
-                Upper r2 = cholqr_device(ctx_, n_, dst, ld_, w, dst, ld_, sync, ortho_bytes);
+                Upper r1 = cholqr_device(ctx_, n_, x, ldx, w, mid, ld_, sync, ortho_bytes);
+                Upper r2 = cholqr_device(ctx_, n_, mid, ld_, w, dst, ld_, sync, ortho_bytes);
                 return tri_mul(r2, r1);
             };
             OrthoRes out;
             if (c0 == 0) {
                 try {
-                    out.r_jj = intra(V, ldv, col(c0));
+                    out.r_jj = intra(V, ldv, s0, col(c0));
                 } catch (const CholFail& f) {
                     throw FirstPassFailure{f.pivot};
                 }
@@ -486,7 +490,7 @@ Store::OrthoRes Store::run_scheme(i64 c0, const double* V, i64 ldv, i64 w, int k
             Upper inner_r;
             try {
                 first_block = project_device(ctx_, n_, col(0), ld_, c0, V, ldv, w, s0, ld_, sync, ortho_bytes);
-                inner_r = intra(s0, ld_, s1);
+                inner_r = intra(s0, ld_, s1, s1);
             } catch (const CholFail& f) {
                 throw FirstPassFailure{f.pivot};
             }

@@ -89,6 +89,21 @@ def main():
         results[name] = {"bitwise": same}
         ok = ok and same
         del op
+    # The default size heuristic (KRY_FUSED_MPK unset) on an odd line count
+    # near its threshold: ranks own 79 / 80 lines at N = 2, and the fused-vs-
+    # per-SpMV choice must be the same on every rank (each rank's halo sends
+    # pair with its neighbour's receives) — bit-identical, and no deadlock.
+    os.environ["KRY_FUSED_MPK"] = "1"
+    a = ref.laplace2d(1000, 159)
+    op = kb.Laplace2D(1000, 159, ctx)
+    start = rng.standard_normal(a.n)
+    want = ref.mpk(a, start, 5)[op.row_begin:op.row_begin + op.n]
+    got = op.mpk(start[op.row_begin:op.row_begin + op.n], 5)
+    same = bool(np.array_equal(got, want))
+    results["mpk_2d1000x159_s5_default_heuristic"] = {"bitwise": same}
+    ok = ok and same
+    del op
+    os.environ["KRY_FUSED_MPK"] = "2"
     # Row-partitioned random-sparse CSR MPK: the segment-pipelined x gather
     # (one broadcast per rank segment, slices aligned to the segments) keeps
     # every row's stored summation order — bit-identical.

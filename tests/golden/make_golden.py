@@ -44,13 +44,30 @@ SOLVER_CONFIGS = [
     ("pip2_2d64_warm", 64, 2, 2, 0, False, "stencil", 0.5, 120),
     ("two_2d200_s60", 200, 2, 3, 60, False, "stencil", None, 500000),
     ("pip2_2d128", 128, 2, 2, 0, False, "stencil", None, 500000),
+    # BASELINE-size configs (round 2).  configs[0] full solves at 512²; a
+    # multi-cycle 3-D golden (64³ needs 3 restarts); configs[1]/[2] as
+    # exactly-k-cycle runs through max_iters = 60k (SURVEY §8(c) "Large configs").
+    ("pip2_2d512", 512, 2, 2, 0, False, "stencil", None, 500000),
+    ("two_2d512_s60", 512, 2, 3, 60, False, "stencil", None, 500000),
+    ("two_3d64_s60", 64, 3, 3, 60, False, "stencil", None, 500000),
+    ("pip2_3d64", 64, 3, 2, 0, False, "stencil", None, 500000),
+    ("two_3d64_s20", 64, 3, 3, 20, False, "stencil", None, 500000),
+    ("two_2d4000_s60_c2", 4000, 2, 3, 60, False, "stencil", None, 120),
+    ("pip2_2d4000_c2", 4000, 2, 2, 0, False, "stencil", None, 120),
+    ("two_2d8000_s60_c1", 8000, 2, 3, 60, False, "stencil", None, 60),
 ]
+# Configs whose CPU reference run takes minutes (generated with --only, merged).
+LARGE = {"pip2_2d512", "two_2d512_s60", "two_2d4000_s60_c2", "pip2_2d4000_c2", "two_2d8000_s60_c1"}
 
 
-def solve_all():
+def solve_all(only=None):
+    import time
     from oracle import ref
     out = {}
     for key, g, dims, kind, shat, standard, opk, x0v, mi in SOLVER_CONFIGS:
+        if only is not None and key not in only:
+            continue
+        t0 = time.perf_counter()
         a = ref.laplace2d(g, g) if dims == 2 else ref.laplace3d(g, g, g)
         b = ref.spmv(a, np.ones(a.n))
         x0 = None if x0v is None else np.full(a.n, x0v)
@@ -66,6 +83,7 @@ def solve_all():
             "initial_residual": rep.initial_residual,
             "final_relative_residual": rep.final_relative_residual,
             "breakdown": rep.breakdown,
+            "reference_seconds": time.perf_counter() - t0,
         }
     return out
 
@@ -133,27 +151,56 @@ def ref_lsq(h, gamma):
 
 
 def main():
+    """python make_golden.py                 all small configs + kernels_golden.npz
+       python make_golden.py --only k1,k2    just these solver configs, merged into solver_golden.json
+       python make_golden.py --large         the LARGE set (minutes to an hour of CPU), merged"""
     if len(sys.argv) > 1 and sys.argv[1] == "--solve-json":
-        print(json.dumps(solve_all()))
+        only = set(sys.argv[2].split(",")) if len(sys.argv) > 2 else None
+        print(json.dumps(solve_all(only)))
         return
+    only = None
+    if len(sys.argv) > 2 and sys.argv[1] == "--only":
+        only = sys.argv[2].split(",")
+    elif len(sys.argv) > 1 and sys.argv[1] == "--large":
+        only = [k for k, *_ in SOLVER_CONFIGS if k in LARGE]
+    elif len(sys.argv) == 1:
+        only = [k for k, *_ in SOLVER_CONFIGS if k not in LARGE]
     subprocess.run(["make", "-C", os.path.join(ROOT, "oracle"), "ref", "ref_fma"], check=True)
-    env = dict(os.environ)
-    res = {}
-    for variant in ("ref", "fma"):
-        env["KRY_REF_VARIANT"] = variant
-        out = subprocess.run([sys.executable, __file__, "--solve-json"], env=env, check=True,
-                             capture_output=True, text=True).stdout
-        res[variant] = json.loads(out)
-    golden = {}
+    path = os.path.join(HERE, "solver_golden.json")
+    golden = json.load(open(path)) if os.path.exists(path) else {}
+    for key in only:
+        # One process per key and variant; the two variants run side by side
+        # unless the store (8·61·n bytes) of two of them would not fit in memory.
+        grid = next(c[1] for c in SOLVER_CONFIGS if c[0] == key)
+        procs = {}
+        for variant in ("ref", "fma"):
+            env = dict(os.environ, KRY_REF_VARIANT=variant)
+            procs[variant] = subprocess.Popen([sys.executable, __file__, "--solve-json", key], env=env,
+                                              stdout=subprocess.PIPE, text=True)
+            if grid >= 8000:
+                procs[variant].wait()
+        res = {}
+        for variant, pr in procs.items():
+            out, _ = pr.communicate()
+            if pr.returncode != 0:
+                raise SystemExit(f"{key}/{variant}: reference run failed ({pr.returncode})")
+            res[variant] = json.loads(out)
+        merge(golden, res)
+        with open(path, "w") as f:
+            json.dump(golden, f, indent=1)
+        print("wrote", key, golden[key]["status"], golden[key]["iterations"], golden[key]["restarts"],
+              f"{golden[key]['reference_seconds']:.1f} s", flush=True)
+    if len(sys.argv) == 1:
+        np.savez_compressed(os.path.join(HERE, "kernels_golden.npz"), **kernels())
+        print("wrote", os.path.join(HERE, "kernels_golden.npz"))
+
+
+def merge(golden, res):
     for key, rep in res["ref"].items():
         fma = res["fma"][key]
         rep["fma_same_counts"] = all(rep[k] == fma[k] for k in ("iterations", "restarts", "reduces"))
         rep["fma_cycle_residuals"] = fma["cycle_residuals"]
         golden[key] = rep
-    with open(os.path.join(HERE, "solver_golden.json"), "w") as f:
-        json.dump(golden, f, indent=1)
-    np.savez_compressed(os.path.join(HERE, "kernels_golden.npz"), **kernels())
-    print("wrote", os.path.join(HERE, "solver_golden.json"), os.path.join(HERE, "kernels_golden.npz"))
 
 
 if __name__ == "__main__":

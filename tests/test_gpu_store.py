@@ -178,7 +178,8 @@ def test_store_config_errors(kb, ctx):
         st.append_block(np.ones((10, 8)), False, kb.OrthoScheme(), kb.SyncCounter())  # capacity
 
 
-@pytest.mark.parametrize("grid,kind,shat", [(64, 2, 0), (64, 3, 60), (100, 3, 20), (128, 3, 60), (128, 2, 0)])
+@pytest.mark.parametrize("grid,kind,shat", [(64, 2, 0), (64, 3, 60), (100, 3, 20), (128, 3, 60), (128, 2, 0),
+                                            (512, 2, 0), (512, 3, 60)])  # 512²: BASELINE configs[0]
 def test_orthogonality_error_protocol(kb, ctx, ref, grid, kind, shat):
     """on the same MPK-fed blocks (one full m = 60 cycle),
     ‖I − QᵀQ‖₂ of the device store is ≤ max(1e-12, 10× the reference

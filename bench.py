@@ -1,15 +1,17 @@
 #!/usr/bin/env python
 """Benchmark of the B200 two-stage s-step GMRES hot path (BASELINE.json metric).
 
-Workload (BASELINE.json configs[1]): 2D Laplace 5-point, 4000×4000 rows per
-GPU (weak scaling: the grid is 4000 × 4000·N for N ranks, row-partitioned by
-whole grid lines), b = A·1, s-step GMRES(60), s = 5, two-stage BlkOrtho with
-ŝ = 60, fp64.  One timed *step* = one full restart cycle through the C ABI
-(kry_sstep_gmres_device with max_iters = 60, warm-started from the current x):
-12 MPK blocks (60 stencil SpMVs), 12 first-stage BCGS-PIP, 1 second-stage
-BCGS-PIP finalize of the 61-column big panel, Hessenberg/LSQ, solution update
-and explicit residual.  Inputs live in HBM (the 7.8 GB/GPU basis is ≫ the
-126 MB L2, so no L2 flush is needed between steps).
+Workload (BASELINE.json configs[2], the north-star config): 2D Laplace
+5-point 8000×8000, row-partitioned by whole grid lines over the N ranks
+(strong scaling: the grid is fixed, N = 1 holds all 64 M rows on one B200),
+b = A·1, s-step GMRES(60), s = 5, two-stage BlkOrtho with ŝ = 60, fp64.
+One timed *step* = one full restart cycle through the C ABI
+(kry_sstep_gmres_device with max_iters = 60, warm-started from the current
+x): 12 MPK blocks (60 stencil SpMVs), 12 first-stage BCGS-PIP, 1
+second-stage BCGS-PIP finalize of the 61-column big panel,
+Hessenberg/LSQ, solution update and explicit residual.  Inputs live in HBM
+(the 31 GB basis is ≫ the 126 MB L2, so no L2 flush is needed between
+steps).  --scaling weak keeps grid² rows per GPU instead (grid × grid·N).
 
 `value` = aggregate BlkOrtho HBM GB/s: Σ_ranks algorithmic BlkOrtho bytes
 (8·n·(2c0+3w) per BCGS-PIP) ÷ BlkOrtho device time (CUDA events
@@ -18,9 +20,10 @@ ranks).  `e2e` = the same bytes ÷ the end-to-end wall time of the same cycles
 through the host-buffer C ABI (kry_sstep_gmres: b and x0 copied H2D from
 pinned memory, x copied D2H, every step).
 
-  python bench.py                      # N=1, 3 warm-up + 5 timed cycles
-  python bench.py --impl reference     # the CPU reference on the same config
+  python bench.py                      # N=1, 3 warm-up + 30 timed cycles at 8000²
+  python bench.py --impl reference     # the CPU reference's BlkOrtho on the same config
   torchrun --nproc-per-node N bench.py --gpus N
+  python bench.py --workload random    # configs[4]: n = 20 M, 30 nnz/row, device Jacobi
 """
 from __future__ import annotations
 
@@ -46,14 +49,17 @@ def parse():
     p.add_argument("--steps", type=int, default=30)
     p.add_argument("--warmup", type=int, default=3)
     p.add_argument("--impl", choices=["ours", "reference"], default="ours")
-    p.add_argument("--grid", type=int, default=4000, help="grid side per GPU (rows per GPU = grid² in 2D)")
+    p.add_argument("--grid", type=int, default=8000,
+                   help="grid side (strong: of the whole grid; weak: per GPU, grid × grid·N)")
+    p.add_argument("--scaling", choices=["strong", "weak"], default="strong",
+                   help="strong (default, BASELINE configs[2]): the grid is split over the ranks")
     p.add_argument("--dims", type=int, choices=[2, 3], default=2, help="2D 5-point or 3D 7-point Laplacian")
     p.add_argument("--workload", choices=["laplace", "random"], default="laplace",
-                   help="random = BASELINE configs[4] (CSR, ~30 nnz/row, Jacobi-scaled)")
-    p.add_argument("--random-rows", type=int, default=20_000_000, help="rows per GPU of the random workload")
+                   help="random = BASELINE configs[4] (kry_gen_random_sparse, 30 nnz/row, device Jacobi)")
+    p.add_argument("--random-rows", type=int, default=20_000_000,
+                   help="rows of the random workload (strong: total; weak: per GPU)")
     p.add_argument("--random-nnz", type=int, default=30)
-    p.add_argument("--global-grid", type=int, default=0,
-                   help="strong scaling: fixed global grid side (e.g. 8000 = BASELINE configs[2]) split over the ranks")
+    p.add_argument("--diag-factor", type=float, default=0.15)
     p.add_argument("--shat", type=int, default=60)
     p.add_argument("--scheme", choices=["two-stage", "bcgs-pip2", "standard"], default="two-stage",
                    help="standard = standard_gmres (gmres.hpp:404: s = 1, CGS2), the paper's GMRES column")
@@ -63,37 +69,6 @@ def parse():
     p.add_argument("--no-e2e", action="store_true")
     p.add_argument("--cpu-sample-blocks", type=int, default=3)
     return p.parse_args()
-
-
-def random_sparse_rows(n_global, row_begin, n_local, per_row, seed=1, chunk=1 << 20):
-    """BASELINE configs[4]: nonsymmetric random sparse rows with `per_row`
-    entries (diagonal + per_row-1 distinct random columns), values uniform in
-    [-1, 1], diagonal 1 + Σ|off-diagonal| (strictly diagonally dominant, so
-    GMRES converges), Jacobi-scaled (each row divided by its diagonal — the
-    reference has no preconditioner hook, so the scaled operator is the
-    problem both solvers see).  Columns strictly increasing per row (CSR
-    contract, csr_matrix.hpp:25-38).  Returns int64 row_ptr (from 0), int64
-    global columns, fp64 values for rows [row_begin, row_begin+n_local)."""
-    import numpy as np
-    k = per_row - 1
-    nnz = n_local * per_row
-    col = np.empty(nnz, dtype=np.int64)
-    val = np.empty(nnz, dtype=np.float64)
-    span = max(1, (n_global - 1) // (k + 1))
-    for c0 in range(0, n_local, chunk):
-        m = min(chunk, n_local - c0)
-        rng = np.random.default_rng([seed, row_begin + c0])
-        rows = np.arange(row_begin + c0, row_begin + c0 + m, dtype=np.int64)[:, None]
-        offs = np.cumsum(rng.integers(1, span + 1, size=(m, k), dtype=np.int64), axis=1)  # distinct, < n_global
-        cols = np.concatenate([(rows + offs) % n_global, rows], axis=1)
-        vals = rng.uniform(-1.0, 1.0, size=(m, k))
-        diag = 1.0 + np.abs(vals).sum(axis=1)
-        vals = np.concatenate([vals / diag[:, None], np.ones((m, 1))], axis=1)
-        order = np.argsort(cols, axis=1, kind="stable")
-        col[c0 * per_row:(c0 + m) * per_row] = np.take_along_axis(cols, order, axis=1).reshape(-1)
-        val[c0 * per_row:(c0 + m) * per_row] = np.take_along_axis(vals, order, axis=1).reshape(-1)
-    row_ptr = np.arange(n_local + 1, dtype=np.int64) * per_row
-    return row_ptr, col, val
 
 
 def peaks():
@@ -160,82 +135,97 @@ class Clocks:
 
 
 # ---------------------------------------------------------------------------------------
-def reference_blkortho_sample(grid, shat, blocks, threads, v_from_gpu=None):
-    """Time the CPU reference's BlkOrtho (BasisStore::preprocess_block) on the
-    first `blocks` blocks of a restart cycle at the bench config.  V blocks are
-    the reference's own MPK on its own CSR (or, for the cpu_baseline leg of our
-    arm, the bit-identical GPU MPK output when `v_from_gpu` is given).
-    Returns (GB/s, seconds, bytes, sample description)."""
+def cpu_slab(grid, dims):
+    """The bounded CPU sample of the bench grid: a slab of whole grid lines
+    (2-D: grid × lines, 3-D: grid × grid × planes) holding about 4 M rows.
+    First-stage BCGS-PIP is row-separable (every Gram entry is a sum over
+    rows, the update is row-local), so the reference's BlkOrtho GB/s on the
+    slab is its rate on the whole grid at 1/k of the time."""
+    plane = grid if dims == 2 else grid * grid
+    lines = max(8, min(grid, (4 << 20) // plane))
+    return lines, lines * plane
+
+
+def reference_blkortho_sample(grid, dims, shat, blocks, threads, first_block=0, store=None):
+    """Time the CPU reference's BlkOrtho (BasisStore::preprocess_block,
+    basis_store.hpp:122-125 → bcgs_pip block_ortho.hpp:180) on blocks
+    [first_block, first_block + blocks) of a restart cycle of the bench
+    configuration, on the cpu_slab rows (the reference's own operator and
+    MPK feed it).  Returns (GB/s, seconds, bytes, description, store)."""
     os.environ["KRYLOV_NUM_THREADS"] = str(threads)
     import numpy as np
     from oracle import ref
 
-    n = grid * grid
+    lines, n = cpu_slab(grid, dims)
     m, s = 60, 5
-    st = ref.Store(n, m, s, shat)
-    if v_from_gpu is None:
-        a = ref.laplace2d(grid, grid)
+    if store is None:
+        a = ref.laplace2d(grid, lines) if dims == 2 else ref.laplace3d(grid, grid, lines)
         b = ref.spmv(a, np.ones(n))
-        mpk = lambda start: ref.mpk(a, start, s)
-    else:
-        b, mpk = v_from_gpu
-    v1 = b / np.linalg.norm(b)
+        store = {"a": a, "v1": b / np.linalg.norm(b), "st": ref.Store(n, m, s, shat)}
+    a, v1, st = store["a"], store["v1"], store["st"]
     secs, byts = 0.0, 0.0
-    for j in range(blocks):
-        start = v1 if j == 0 else st.column(st.info().filled - 1)
-        blk = mpk(start)
-        c0 = 0 if j == 0 else st.info().filled - 1
-        t = time.perf_counter()
-        st.preprocess_block(blk, j != 0)
-        secs += time.perf_counter() - t
-        byts += 8.0 * n * (2 * c0 + 3 * (s + 1))
-    desc = (f"CPU reference BasisStore::preprocess_block (first-stage BCGS-PIP), blocks 0..{blocks - 1} "
-            f"of a restart cycle at {grid}x{grid} (n={n}), KRYLOV_NUM_THREADS={threads}")
-    return byts / secs / 1e9, secs, byts, desc
-
-
-def run_reference(args):
-    rank = int(os.environ.get("RANK", "0"))
-    if rank != 0:
-        return 0
-    threads = os.cpu_count() or 1
-    K, W = args.steps, args.warmup
-    # One step = one first-stage BCGS-PIP of the reference at the bench config
-    # (a full CPU restart cycle at 4000² takes minutes; SURVEY §6).
-    import numpy as np
-    from oracle import ref
-    os.environ["KRYLOV_NUM_THREADS"] = str(threads)
-    g = args.grid
-    n = g * g
-    a = ref.laplace2d(g, g)
-    b = ref.spmv(a, np.ones(n))
-    st = ref.Store(n, 60, 5, args.shat)
-    v1 = b / np.linalg.norm(b)
-    times, byts = [], []
-    for k in range(W + K):
+    for k in range(first_block, first_block + blocks):
         info = st.info()
-        if info.filled + 5 > 61:
+        if info.filled + s > m + 1:  # a new restart cycle
             st.reset()
             info = st.info()
         start = v1 if info.filled == 0 else st.column(info.filled - 1)
-        blk = ref.mpk(a, start, 5)
+        blk = ref.mpk(a, start, s)
         c0 = 0 if info.filled == 0 else info.filled - 1
         t = time.perf_counter()
         st.preprocess_block(blk, info.filled != 0)
-        dt = time.perf_counter() - t
+        secs += time.perf_counter() - t
+        byts += 8.0 * n * (2 * c0 + 3 * (s + 1))
+    shape = f"{grid}x{lines}" if dims == 2 else f"{grid}x{grid}x{lines}"
+    desc = (f"CPU reference BasisStore::preprocess_block (first-stage BCGS-PIP, c0 cycling 0..55 as in a restart "
+            f"cycle), {blocks} blocks on a {shape} slab of whole grid lines (n={n}) of the bench grid, "
+            f"KRYLOV_NUM_THREADS={threads}")
+    return byts / secs / 1e9, secs, byts, desc, store
+
+
+def run_reference(args):
+    """The reference arm: the unmodified CPU reference (oracle/_ref, built from
+    /root/reference) on this box's host cores, same metric and unit (BlkOrtho
+    GB/s).  One step = one first-stage BCGS-PIP block on the cpu_slab sample
+    of the bench grid (a full 8000² cycle takes minutes on the CPU, SURVEY
+    §6).  KRYLOV_NUM_THREADS: both 1 and all host threads are probed and the
+    faster is timed (the reference's SpMV gets slower with threads, SURVEY
+    A.5); both probes are recorded."""
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return 0
+    K, W = args.steps, args.warmup
+    g, dims = args.grid, args.dims
+    nproc = os.cpu_count() or 1
+    probes = {}
+    for th in sorted({1, nproc}):
+        gbs, secs, _, _, _ = reference_blkortho_sample(g, dims, args.shat, 3, th)
+        probes[th] = gbs
+    threads = max(probes, key=probes.get)
+    store = None
+    times, byts = [], []
+    for k in range(W + K):
+        gbs, secs, b, desc, store = reference_blkortho_sample(g, dims, args.shat, 1, threads, k, store)
         if k >= W:
-            times.append(dt)
-            byts.append(8.0 * n * (2 * c0 + 18))
+            times.append(secs)
+            byts.append(b)
     total = sum(times)
     value = sum(byts) / total / 1e9
+    lines, n = cpu_slab(g, dims)
+    shape = f"{g}x{g}" if dims == 2 else f"{g}x{g}x{g}"
     line = {
         "impl": "reference", "metric": METRIC, "value": value, "unit": "GB/s", "n_gpus": args.gpus,
-        "steps": K, "warmup": W, "ms_per_step": 1e3 * total / K, "higher_is_better": True, "scaling": "weak",
-        "vs_baseline": None, "dtype": "f64", "data": "synthetic",
-        "config": {"workload": f"2D Laplace 5-pt {g}x{g}, s-step GMRES(60) s=5, two-stage BlkOrtho shat={args.shat}",
-                   "grid": [g, g], "rows": n, "step": "one first-stage BCGS-PIP (BasisStore::preprocess_block)"},
+        "steps": K, "warmup": W, "ms_per_step": 1e3 * total / K, "higher_is_better": True,
+        "scaling": args.scaling, "vs_baseline": None, "dtype": "f64", "data": "synthetic",
+        "config": {"workload": f"{'2D Laplace 5-pt' if dims == 2 else '3D Laplace 7-pt'} {shape}, s-step GMRES(60) "
+                               f"s=5, two-stage BlkOrtho shat={args.shat}",
+                   "grid": [g, g] if dims == 2 else [g, g, g], "sample_rows": n,
+                   "step": "one first-stage BCGS-PIP (BasisStore::preprocess_block) on a slab of whole grid lines "
+                           "of the bench grid (BlkOrtho is row-separable; the GB/s rate is the metric)"},
         "cpu_baseline": {"value": value, "unit": "GB/s", "cores": threads, "kind": "reference",
-                         "sample": f"{K} first-stage BCGS-PIP blocks at {g}x{g} (after {W} warm-up blocks)"},
+                         "sample": f"{K} first-stage BCGS-PIP blocks (c0 cycling as in a restart cycle) on "
+                                   f"{n} rows of the {shape} grid after {W} warm-up blocks",
+                         "threads_probed_gbs": {str(k): v for k, v in probes.items()}},
         "e2e": {"value": value, "unit": "GB/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0},
     }
     print(json.dumps(line), flush=True)
@@ -269,21 +259,24 @@ def run_ours(args):
     stream = torch.cuda.ExternalStream(ctx.stream_handle())
 
     g = args.grid
-    strong = args.global_grid > 0
+    strong = args.scaling == "strong"
     if args.workload == "random":
-        nl = args.random_rows
-        n_glob = nl * world
-        rp, ci, vv = random_sparse_rows(n_glob, rank * nl, nl, args.random_nnz)
-        op = kb.CsrOperator(rp, ci, vv, n_global=n_glob, row_begin=rank * nl, ctx=ctx)
-        del rp, ci, vv
+        # configs[4]: rows of the generator (kry_gen_random_sparse, SplitMix64
+        # seed 1), b = A·1 of the unscaled matrix, then device Jacobi.
+        n_glob = args.random_rows if strong else args.random_rows * world
+        rb, re = rank * n_glob // world, (rank + 1) * n_glob // world
+        op = kb.CsrOperator(*kb.gen_random_sparse(n_glob, rb, re - rb, args.random_nnz, seed=1,
+                                                  diag_factor=args.diag_factor),
+                            n_global=n_glob, row_begin=rb, ctx=ctx)
         nx, ny, nz = n_glob, 1, 1
-        shape = f"random sparse n={n_glob} ({args.random_nnz} nnz/row, Jacobi-scaled)"
+        shape = (f"random sparse n={n_glob} ({args.random_nnz} nnz/row, SplitMix64 seed 1, "
+                 f"diag 1+{args.diag_factor}*sum|off|, device Jacobi)")
     elif args.dims == 2:
-        nx, ny, nz = (args.global_grid, args.global_grid, 1) if strong else (g, g * world, 1)
+        nx, ny, nz = (g, g, 1) if strong else (g, g * world, 1)
         op = kb.Laplace2D(nx, ny, ctx)
         shape = f"2D Laplace 5-pt {nx}x{ny}"
     else:
-        nx, ny, nz = (args.global_grid,) * 3 if strong else (g, g, g * world)
+        nx, ny, nz = (g, g, g) if strong else (g, g, g * world)
         op = kb.Laplace3D(nx, ny, nz, ctx)
         shape = f"3D Laplace 7-pt {nx}x{ny}x{nz}"
     n = op.n
@@ -298,6 +291,8 @@ def run_ours(args):
     x = torch.zeros(n, dtype=torch.float64, device="cuda")
     torch.cuda.synchronize()
     kb.lib().kry_spmv_device(ctx.handle, op.handle, ones.data_ptr(), b.data_ptr())  # b = A·1 (gen_rhs_ones)
+    if args.workload == "random":
+        op.jacobi()  # from here the operator is D⁻¹A; the solver forms D⁻¹b on the device
 
     def barrier():
         torch.cuda.synchronize()
@@ -391,22 +386,15 @@ def run_ours(args):
         try:
             with open(tpath) as f:
                 tj = json.load(f)
-            key = f"{dom}@{nx}x{g}" if args.dims == 2 and not strong else f"{dom}@{shape}/{world}"
-            traffic = tj.get(key)
+            traffic = tj.get(f"{dom}@{shape}/{world}")
         except Exception:
             traffic = None
 
     cpu = None
-    if (rank == 0 and world == 1 and not args.no_cpu_baseline and args.dims == 2 and not strong
-            and args.workload == "laplace"):
-        def gpu_mpk(start):
-            return op.mpk(start, 5)
-        bh = b.cpu().numpy()
-        gbs, secs, byts, desc = reference_blkortho_sample(g, args.shat, args.cpu_sample_blocks, 1,
-                                                          v_from_gpu=(bh, gpu_mpk))
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.workload == "laplace":
+        gbs, secs, byts, desc, _ = reference_blkortho_sample(g, args.dims, args.shat, args.cpu_sample_blocks, 1)
         cpu = {"value": gbs, "unit": "GB/s", "cores": 1, "kind": "reference",
-               "sample": desc + f"; {secs:.1f} s of CPU BlkOrtho ({byts / 1e9:.1f} GB algorithmic); V blocks "
-                                "from the bit-identical GPU MPK"}
+               "sample": desc + f"; {secs:.1f} s of CPU BlkOrtho ({byts / 1e9:.1f} GB algorithmic)"}
 
     # Time to solution at BASELINE config 1 (2D Laplace 512², tol 1e-6): full
     # solves from x0 = 0, one-stage BCGS-PIP2 (the CPU reference's config) and

@@ -175,6 +175,32 @@ int kry_laplace_partition(int dims, int64_t nx, int64_t ny, int64_t nz, int nran
 int kry_operator_destroy(kry_operator* op);
 int kry_operator_rows(const kry_operator* op, int64_t* n_global, int64_t* row_begin, int64_t* n_local);
 int kry_operator_nnz(const kry_operator* op, int64_t* nnz_local);
+/* Left Jacobi preconditioning (the reference has no
+ * preconditioner hook, gmres.hpp:80-90).  From this call on the
+ * operator is D⁻¹A, D = diag(A): the CSR values are divided by their row's
+ * diagonal in place on the device (IEEE division, so the operator is
+ * bit-identical to a host pre-scaling a_ij / a_ii), kry_spmv/kry_mpk apply
+ * D⁻¹A, and the solvers take the ORIGINAL b and solve D⁻¹A x = D⁻¹b (D⁻¹b
+ * formed on the device; residual histories are those of the scaled
+ * system, exactly what the reference reports when handed D⁻¹A and D⁻¹b).
+ * Irreversible; calling it twice is a no-op.  KRY_INVALID_ARGUMENT if a row
+ * has no (or a zero) diagonal entry; KRY_UNSUPPORTED for the matrix-free
+ * Laplacians unless built with stencil Jacobi. */
+int kry_operator_jacobi(kry_operator* op);
+int kry_operator_is_jacobi(const kry_operator* op, int* enabled);
+/* Host-only generator of the BASELINE configs[4] workload: rows
+ * [row_begin, row_begin + n_local) of an n_global×n_global nonsymmetric
+ * random sparse matrix with per_row entries per row (the diagonal and
+ * per_row − 1 distinct random columns), built on the reference's SplitMix64
+ * (rng.hpp:19-42) — a function of (n_global, per_row, seed, diag_factor)
+ * only, whatever the rank layout.  Off-diagonal values uniform in [−1, 1),
+ * a_ii = 1 + diag_factor·Σ|a_ij| (diag_factor 0.15: GMRES(60) restarts
+ * 5-6 times at tol 1e-6); jacobi != 0 returns D⁻¹A instead.  row_ptr has
+ * n_local+1 entries from 0 (row_ptr[i] = i·per_row), col_idx/vals
+ * n_local·per_row, ascending columns per row.  Multithreaded.  The numpy
+ * restatement is oracle/randsparse.py. */
+int kry_gen_random_sparse(int64_t n_global, int64_t row_begin, int64_t n_local, int64_t per_row, uint64_t seed,
+                          double diag_factor, int jacobi, int64_t* row_ptr, int64_t* col_idx, double* vals);
 /* y = A·x for this rank's rows (spmv, csr_matrix.hpp:69). Host buffers. */
 int kry_spmv(kry_ctx* ctx, kry_operator* op, const double* x, double* y);
 /* Device buffers (ld irrelevant: vectors). */

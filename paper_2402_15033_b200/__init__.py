@@ -356,6 +356,18 @@ class Operator:
         _check(lib().kry_mpk(self.ctx.handle, self._h, _p(start), s, _p(v)))
         return v
 
+    def jacobi(self) -> "Operator":
+        """Left Jacobi preconditioning on the device: from now on this operator
+        is D⁻¹A and solves take the original b (kry_operator_jacobi)."""
+        _check(lib().kry_operator_jacobi(self._h))
+        return self
+
+    @property
+    def is_jacobi(self) -> bool:
+        e = C.c_int()
+        _check(lib().kry_operator_is_jacobi(self._h, C.byref(e)))
+        return bool(e.value)
+
     def close(self):
         if self._h:
             lib().kry_operator_destroy(self._h)
@@ -387,6 +399,20 @@ class CsrOperator(Operator):
         self._h = h
         self._rows()
         self.nnz = int(rp[-1])
+
+
+def gen_random_sparse(n_global: int, row_begin: int = 0, n_local: Optional[int] = None, per_row: int = 30,
+                      seed: int = 1, diag_factor: float = 0.15, jacobi: bool = False):
+    """BASELINE configs[4] rows on the host (kry_gen_random_sparse): int64
+    row_ptr (from 0), int64 global columns, fp64 values."""
+    n_local = n_global - row_begin if n_local is None else n_local
+    rp = np.empty(n_local + 1, dtype=np.int64)
+    ci = np.empty(n_local * per_row, dtype=np.int64)
+    vv = np.empty(n_local * per_row, dtype=np.float64)
+    _check(lib().kry_gen_random_sparse(n_global, row_begin, n_local, per_row, seed, diag_factor, int(jacobi),
+                                       rp.ctypes.data_as(P_i64), ci.ctypes.data_as(P_i64),
+                                       vv.ctypes.data_as(P_dbl)))
+    return rp, ci, vv
 
 
 class Laplace2D(Operator):

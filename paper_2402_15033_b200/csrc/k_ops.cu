@@ -773,4 +773,86 @@ void launch_xupdate(cudaStream_t s, i64 n, const double* x, const double* Q, i64
     ++launches;
 }
 
+// ---- Jacobi (left diagonal scaling) ------------------------------
+// D⁻¹A is formed once on the device, in place over the operator's values
+// (every entry divided by its row's diagonal, an IEEE division: bit for bit
+// what a host pre-scaling a_ij / a_ii gives the reference); D⁻¹b per solve.
+namespace {
+template <typename RP>
+__global__ void __launch_bounds__(kBlock) csr_find_diag_kernel(i64 nloc, const RP* __restrict__ rp,
+                                                               const int32_t* __restrict__ col,
+                                                               const double* __restrict__ vals, i64 diag_col0,
+                                                               double* __restrict__ d) {
+    KB_PDL_WAIT();
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nloc; i += (i64)gridDim.x * blockDim.x) {
+        const i64 dc = diag_col0 + i;
+        for (i64 k = rp[i]; k < static_cast<i64>(rp[i + 1]); ++k)
+            if (col[k] == dc) d[i] = vals[k];
+    }
+}
+
+template <typename RP>
+__global__ void __launch_bounds__(kBlock) csr_scale_rows_kernel(i64 nloc, const RP* __restrict__ rp,
+                                                                double* __restrict__ vals,
+                                                                const double* __restrict__ d) {
+    KB_PDL_WAIT();
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < nloc; i += (i64)gridDim.x * blockDim.x) {
+        const double di = d[i];
+        for (i64 k = rp[i]; k < static_cast<i64>(rp[i + 1]); ++k) vals[k] = __ddiv_rn(vals[k], di);
+    }
+}
+
+__global__ void __launch_bounds__(kBlock) count_zero_kernel(i64 n, const double* __restrict__ d,
+                                                            unsigned long long* __restrict__ zeros) {
+    KB_PDL_WAIT();
+    unsigned long long c = 0;
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        c += (d[i] == 0.0 || !(d[i] == d[i])) ? 1ull : 0ull;
+    if (c) atomicAdd(zeros, c);
+}
+
+__global__ void __launch_bounds__(kBlock) div_diag_kernel(i64 n, const double* __restrict__ b,
+                                                          const double* __restrict__ d, double dconst,
+                                                          double* __restrict__ out) {
+    KB_PDL_WAIT();
+    for (i64 i = blockIdx.x * (i64)blockDim.x + threadIdx.x; i < n; i += (i64)gridDim.x * blockDim.x)
+        out[i] = __ddiv_rn(b[i], d ? d[i] : dconst);
+}
+}  // namespace
+
+void launch_csr_find_diag(cudaStream_t s, i64 nloc, const int64_t* rp64, const int32_t* rp32, const int32_t* col,
+                          const double* vals, i64 diag_col0, double* d, int64_t& launches) {
+    const int grid = grid_for(nloc);
+    if (rp64)
+        launch_pdl(csr_find_diag_kernel<int64_t>, grid, kBlock, 0, s, nloc, rp64, col, vals, diag_col0, d);
+    else
+        launch_pdl(csr_find_diag_kernel<int32_t>, grid, kBlock, 0, s, nloc, rp32, col, vals, diag_col0, d);
+    KB_LAUNCHED();
+    ++launches;
+}
+
+void launch_csr_scale_rows(cudaStream_t s, i64 nloc, const int64_t* rp64, const int32_t* rp32, double* vals,
+                           const double* d, int64_t& launches) {
+    const int grid = grid_for(nloc);
+    if (rp64)
+        launch_pdl(csr_scale_rows_kernel<int64_t>, grid, kBlock, 0, s, nloc, rp64, vals, d);
+    else
+        launch_pdl(csr_scale_rows_kernel<int32_t>, grid, kBlock, 0, s, nloc, rp32, vals, d);
+    KB_LAUNCHED();
+    ++launches;
+}
+
+void launch_count_zero(cudaStream_t s, i64 n, const double* d, unsigned long long* zeros, int64_t& launches) {
+    launch_pdl(count_zero_kernel, grid_for(n), kBlock, 0, s, n, d, zeros);
+    KB_LAUNCHED();
+    ++launches;
+}
+
+void launch_div_diag(cudaStream_t s, i64 n, const double* b, const double* d, double dconst, double* out,
+                     int64_t& launches) {
+    launch_pdl(div_diag_kernel, grid_for(n), kBlock, 0, s, n, b, d, dconst, out);
+    KB_LAUNCHED();
+    ++launches;
+}
+
 }  // namespace kb

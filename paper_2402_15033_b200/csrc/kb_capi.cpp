@@ -349,6 +349,22 @@ int kry_operator_nnz(const kry_operator* op, int64_t* nnz_local) {
     return guarded([&] { *nnz_local = op->op->nnz_local; });
 }
 
+int kry_operator_jacobi(kry_operator* op) {
+    return guarded([&] { op->op->set_jacobi(); });
+}
+
+int kry_operator_is_jacobi(const kry_operator* op, int* enabled) {
+    return guarded([&] { *enabled = op->op->jacobi ? 1 : 0; });
+}
+
+int kry_gen_random_sparse(int64_t n_global, int64_t row_begin, int64_t n_local, int64_t per_row, uint64_t seed,
+                          double diag_factor, int jacobi, int64_t* row_ptr, int64_t* col_idx, double* vals) {
+    return guarded([&] {
+        kb::gen_random_sparse(n_global, row_begin, n_local, per_row, seed, diag_factor, jacobi != 0, row_ptr,
+                              col_idx, vals);
+    });
+}
+
 int kry_spmv_device(kry_ctx* ctx, kry_operator* op, const double* d_x, double* d_y) {
     return guarded([&] {
         kb::Ctx& c = C(ctx);

@@ -37,7 +37,7 @@ Workspace::~Workspace() {
     if (copy_stream) cudaStreamDestroy(copy_stream);
 }
 
-Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, const kry_solver_config& cfg_in,
+Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, const kry_solver_config& cfg_in,
              bool standard_mode, double* d_x_out, Workspace* ws, double* h_x_out) {
     kry_solver_config cfg = cfg_in;
     if (standard_mode) {  // standard_gmres (gmres.hpp:404-411)
@@ -69,6 +69,8 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b, const double* d_x0, cons
         W.shat = shat;
     }
     DevBuf &x = W.x, &xn = W.xn, &r = W.r, &rn = W.rn;
+    // Left Jacobi: the operator is D⁻¹A, the system D⁻¹A x = D⁻¹b.
+    const double* d_b = op.scaled_rhs(d_b_in, W.bj);
     x.ensure(vbytes);
     xn.ensure(vbytes);
     r.ensure(vbytes);

@@ -36,6 +36,7 @@ struct Workspace {
     i64 n = -1, m = -1, s = -1, shat = -1;
     std::unique_ptr<Store> store;
     DevBuf x, xn, r, rn;
+    DevBuf bj;  // D⁻¹b of a Jacobi-preconditioned operator
     // host-output path: the solution update streams to the host while it is
     // computed (side stream, one event per row chunk)
     cudaStream_t copy_stream = nullptr;

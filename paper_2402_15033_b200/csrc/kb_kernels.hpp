@@ -97,6 +97,16 @@ int launch_csr_sliced(cudaStream_t s, i64 nloc, int nslices, const int32_t* cons
                       const int32_t* const* col, const double* const* vals, const double* x, const double* b,
                       double* y, double* partials, double* part_sum, int64_t& launches);
 int reduce_grid();  // fixed grid of every partial-sum kernel (determinism)
+// Jacobi (D⁻¹A formed in place on the device; D⁻¹b per solve).  One of
+// rp64 / rp32 is non-null (unsliced CSR / one column slice).
+void launch_csr_find_diag(cudaStream_t s, i64 nloc, const int64_t* rp64, const int32_t* rp32, const int32_t* col,
+                          const double* vals, i64 diag_col0, double* d, int64_t& launches);
+void launch_csr_scale_rows(cudaStream_t s, i64 nloc, const int64_t* rp64, const int32_t* rp32, double* vals,
+                           const double* d, int64_t& launches);
+void launch_count_zero(cudaStream_t s, i64 n, const double* d, unsigned long long* zeros, int64_t& launches);
+// out = b / d (d == nullptr: b / dconst), IEEE division.
+void launch_div_diag(cudaStream_t s, i64 n, const double* b, const double* d, double dconst, double* out,
+                     int64_t& launches);
 
 // ---- k_fused.cu : K6 fused first-stage pass (update j → MPK j+1 → Gram j+1)
 struct FusedPassArgs {

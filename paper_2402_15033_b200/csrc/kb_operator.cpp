@@ -266,6 +266,50 @@ bool Operator::mpk(const double* x, double* out, i64 ldo, int s) {
     return true;
 }
 
+void Operator::set_jacobi() {
+    if (jacobi) return;
+    Ctx& c = *ctx;
+    if (kind != CSR)
+        fail(KRY_UNSUPPORTED, "Jacobi scaling is implemented for CSR operators (the Laplacians' diagonal is constant)");
+    diag.ensure(static_cast<size_t>(std::max<i64>(nloc, 1)) * 8);
+    KB_CUDA(cudaMemsetAsync(diag.p, 0, static_cast<size_t>(std::max<i64>(nloc, 1)) * 8, c.stream));
+    // the diagonal of local row i is gathered column (rank·max_rows + i)
+    // with several ranks, global column row_begin + i with one
+    const i64 dc0 = c.nranks > 1 ? static_cast<i64>(c.rank) * max_rows : row_begin;
+    if (nslices >= 2) {
+        for (int p = 0; p < nslices; ++p)
+            launch_csr_find_diag(c.stream, nloc, nullptr, s_row_ptr[p].as<int32_t>(), s_col[p].as<int32_t>(),
+                                 s_vals[p].p, dc0, diag.p, c.launches);
+    } else {
+        launch_csr_find_diag(c.stream, nloc, row_ptr.as<int64_t>(), nullptr, col.as<int32_t>(), vals.p, dc0, diag.p,
+                             c.launches);
+    }
+    DevBuf cnt;
+    cnt.ensure(8);
+    KB_CUDA(cudaMemsetAsync(cnt.p, 0, 8, c.stream));
+    launch_count_zero(c.stream, nloc, diag.p, reinterpret_cast<unsigned long long*>(cnt.p), c.launches);
+    unsigned long long zeros = 0;
+    KB_CUDA(cudaMemcpyAsync(&zeros, cnt.p, 8, cudaMemcpyDeviceToHost, c.stream));
+    c.sync();
+    if (zeros) fail(KRY_INVALID_ARGUMENT, "Jacobi needs a nonzero diagonal entry in every row");
+    if (nslices >= 2) {
+        for (int p = 0; p < nslices; ++p)
+            launch_csr_scale_rows(c.stream, nloc, nullptr, s_row_ptr[p].as<int32_t>(), s_vals[p].p, diag.p,
+                                  c.launches);
+    } else {
+        launch_csr_scale_rows(c.stream, nloc, row_ptr.as<int64_t>(), nullptr, vals.p, diag.p, c.launches);
+    }
+    c.sync();
+    jacobi = true;
+}
+
+const double* Operator::scaled_rhs(const double* b, DevBuf& buf) {
+    if (!jacobi) return b;
+    buf.ensure(static_cast<size_t>(std::max<i64>(nloc, 1)) * 8);
+    launch_div_diag(ctx->stream, nloc, b, diag.p, 0.0, buf.p, ctx->launches);
+    return buf.p;
+}
+
 double Operator::bytes_per_apply() const {
     if (kind == CSR) return 12.0 * nnz_local + 8.0 * (nloc + 1) + 16.0 * nloc;
     return 16.0 * nloc;

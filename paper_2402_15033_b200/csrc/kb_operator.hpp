@@ -41,7 +41,17 @@ struct Operator {
     DevBuf mpk_lo, mpk_hi;    // s-line halos of the fused MPK
     // bytes moved by one application (algorithmic)
     double bytes_per_apply() const;
+    // Left Jacobi preconditioning: once set, the operator IS
+    // D⁻¹A (CSR: the values divided by their row's diagonal in place on the
+    // device), and solves scale b to D⁻¹b on the device (scaled_rhs).
+    bool jacobi = false;
+    DevBuf diag;              // CSR: a_ii per local row
+    void set_jacobi();
+    // D⁻¹b into buf (the caller's b when the operator is not preconditioned).
+    const double* scaled_rhs(const double* b, DevBuf& buf);
 };
+void gen_random_sparse(i64 n_global, i64 row_begin, i64 n_local, i64 per_row, uint64_t seed, double diag_factor,
+                       bool jacobi, int64_t* row_ptr, int64_t* col, double* vals);
 
 void laplace_partition(int dims, i64 nx, i64 ny, i64 nz, int nranks, int rank, i64& row_begin, i64& nloc,
                        i64& halo);

@@ -26,7 +26,8 @@ os.environ["KRY_FUSED_MPK"] = "2"
 
 GOLDEN = json.load(open(os.path.join(ROOT, "tests", "golden", "solver_golden.json")))
 CONFIGS = ["two_2d100_s60", "two_2d100_s20", "pip2_2d64", "two_3d16_s60", "two_2d48_csr", "standard_2d32",
-           "two_2d128_s60"]
+           "two_2d128_s60", "two_3d64_s60", "rand20k_two_s60_jac", "two_2d512_s60"]
+CONFIGS = [k for k in CONFIGS if k in GOLDEN]
 
 
 def main():
@@ -44,7 +45,13 @@ def main():
     for key in CONFIGS:
         g = GOLDEN[key]
         grid = g["grid"]
-        if g["operator"] == "csr":
+        if g["operator"] == "random":  # configs[4] rows of this rank, device Jacobi
+            rb, re = rank * grid // world, (rank + 1) * grid // world
+            op = kb.CsrOperator(*kb.gen_random_sparse(grid, rb, re - rb, 30, seed=1, diag_factor=0.15),
+                                n_global=grid, row_begin=rb, ctx=ctx)
+            b = op.spmv(np.ones(op.n))
+            op.jacobi()
+        elif g["operator"] == "csr":
             from oracle import ref
             a = ref.laplace2d(grid, grid)
             n = a.n
@@ -57,7 +64,8 @@ def main():
             op = kb.Laplace2D(grid, grid, ctx)
         else:
             op = kb.Laplace3D(grid, grid, grid, ctx)
-        b = op.spmv(np.ones(op.n))
+        if g["operator"] != "random":
+            b = op.spmv(np.ones(op.n))
         cfg = kb.SolverConfig(scheme=kb.OrthoScheme(kb.OrthoKind(g["kind"]), g["shat"]), big_step=g["shat"],
                               max_iters=g["max_iters"])
         rep = kb.standard_gmres(op, b, None, cfg) if g["standard"] else kb.sstep_gmres(op, b, None, cfg)
@@ -122,6 +130,18 @@ def main():
     got = op.mpk(start[rb:re], 5)
     same = bool(np.array_equal(got, want))
     results["mpk_csr_random6000_s5"] = {"bitwise": same}
+    ok = ok and same
+    del op
+    # Row-partitioned Jacobi (configs[4] generator rows of this rank, D⁻¹A
+    # formed on the device): bit-identical to the pre-scaled reference MPK.
+    from oracle import randsparse
+    n = 9000
+    rb, re = rank * n // world, (rank + 1) * n // world
+    op = kb.CsrOperator(*kb.gen_random_sparse(n, rb, re - rb, 30), n_global=n, row_begin=rb, ctx=ctx).jacobi()
+    a = ref.Csr(n, *randsparse.random_sparse(n, 0, n, 30, 1, 0.15, jacobi=True))
+    start = rng.standard_normal(n)
+    same = bool(np.array_equal(op.mpk(start[rb:re], 5), ref.mpk(a, start, 5)[rb:re]))
+    results["mpk_csr_jacobi9000_s5"] = {"bitwise": same}
     ok = ok and same
     del op
     line = json.dumps({"rank": rank, "world": world, "ok": ok, "results": results})

@@ -55,6 +55,13 @@ SOLVER_CONFIGS = [
     ("two_2d4000_s60_c2", 4000, 2, 3, 60, False, "stencil", None, 120),
     ("pip2_2d4000_c2", 4000, 2, 2, 0, False, "stencil", None, 120),
     ("two_2d8000_s60_c1", 8000, 2, 3, 60, False, "stencil", None, 60),
+    # BASELINE configs[4] at n = 20,000 (grid = n): the random-sparse
+    # generator (oracle/randsparse.py ≡ kry_gen_random_sparse, diag_factor
+    # 0.15, 30 entries per row), Jacobi-scaled: the reference is handed D⁻¹A
+    # and D⁻¹b with b = A·1 (5-6 restarts).
+    ("rand20k_two_s60_jac", 20000, 0, 3, 60, False, "random", None, 500000),
+    ("rand20k_pip2_jac", 20000, 0, 2, 0, False, "random", None, 500000),
+    ("rand20k_two_s20_jac", 20000, 0, 3, 20, False, "random", None, 500000),
 ]
 # Configs whose CPU reference run takes minutes (generated with --only, merged).
 LARGE = {"pip2_2d512", "two_2d512_s60", "two_2d4000_s60_c2", "pip2_2d4000_c2", "two_2d8000_s60_c1"}
@@ -68,8 +75,11 @@ def solve_all(only=None):
         if only is not None and key not in only:
             continue
         t0 = time.perf_counter()
-        a = ref.laplace2d(g, g) if dims == 2 else ref.laplace3d(g, g, g)
-        b = ref.spmv(a, np.ones(a.n))
+        if opk == "random":
+            a, b = random_jacobi_system(g)
+        else:
+            a = ref.laplace2d(g, g) if dims == 2 else ref.laplace3d(g, g, g)
+            b = ref.spmv(a, np.ones(a.n))
         x0 = None if x0v is None else np.full(a.n, x0v)
         rep = ref.solve(a, b, x0, ref.make_config(kind=kind, big_step=shat, shat=shat, max_iters=mi),
                         standard=standard)
@@ -86,6 +96,18 @@ def solve_all(only=None):
             "reference_seconds": time.perf_counter() - t0,
         }
     return out
+
+
+def random_jacobi_system(n, per_row=30, seed=1, diag_factor=0.15):
+    """(D⁻¹A, D⁻¹b), b = A·1, of the configs[4] generator — what the device
+    path computes with kry_operator_jacobi on A and the original b."""
+    from oracle import ref, randsparse
+    rp, ci, vv = randsparse.random_sparse(n, 0, n, per_row, seed, diag_factor)
+    a = ref.Csr(n, rp, ci, vv)
+    b = ref.spmv(a, np.ones(n))
+    d = vv[np.nonzero(ci == np.repeat(np.arange(n), np.diff(rp)))[0]]
+    rps, cis, vvs = randsparse.random_sparse(n, 0, n, per_row, seed, diag_factor, jacobi=True)
+    return ref.Csr(n, rps, cis, vvs), b / d
 
 
 def kernels():

@@ -250,3 +250,31 @@ def test_pip_partial_reports_partial_factor(kb, ctx, ref, rng):
     assert out.bad_pivot == piv
     assert out.q is None
     assert rel(out.r_col, rc) < 1e-12
+
+
+# ---- Jacobi: D⁻¹A formed on the device ------------------------------
+@pytest.mark.parametrize("n,slices", [(20000, 1), (20000, 3), (333, 2)])
+def test_jacobi_csr_bitwise(kb, ctx, ref, rng, monkeypatch, n, slices):
+    """kry_operator_jacobi on the configs[4] matrix: SpMV and MPK bit-identical
+    to the reference's spmv / mpk_monomial on the host pre-scaled D⁻¹A
+    (csr_matrix.hpp:69-79, gmres.hpp:80-90), unsliced and column-sliced."""
+    from oracle import randsparse
+    monkeypatch.setenv("KRY_CSR_SLICES", str(slices))
+    op = kb.CsrOperator(*kb.gen_random_sparse(n, per_row=min(30, n)))
+    assert not op.is_jacobi
+    op.jacobi()
+    op.jacobi()  # idempotent
+    assert op.is_jacobi
+    a = ref.Csr(n, *randsparse.random_sparse(n, 0, n, min(30, n), 1, 0.15, jacobi=True))
+    x = rng.standard_normal(n)
+    np.testing.assert_array_equal(op.spmv(x), ref.spmv(a, x))
+    np.testing.assert_array_equal(op.mpk(x, 5), ref.mpk(a, x, 5))
+
+
+def test_jacobi_rejects_missing_diagonal(kb, ctx, rng):
+    # row 1 has no diagonal entry: refused, and the operator is left unscaled
+    op = kb.CsrOperator(np.array([0, 2, 3]), np.array([0, 1, 0]), np.array([2.0, 1.0, 1.0]))
+    with pytest.raises(ValueError):
+        op.jacobi()
+    assert not op.is_jacobi
+    np.testing.assert_array_equal(op.spmv(np.array([1.0, 1.0])), np.array([3.0, 1.0]))

@@ -34,14 +34,19 @@ def cycle_tolerance(g):
 def run_golden(kb, ref, key):
     g = GOLDEN[key]
     grid, dims = g["grid"], g["dims"]
-    if g["operator"] == "csr":
-        a = ref.laplace2d(grid, grid)
-        op = kb.CsrOperator(a.row_ptr, a.col_idx, a.vals)
-    elif dims == 2:
-        op = kb.Laplace2D(grid, grid)
+    if g["operator"] == "random":  # BASELINE configs[4]: generator + device Jacobi (grid = n)
+        op = kb.CsrOperator(*kb.gen_random_sparse(grid, per_row=30, seed=1, diag_factor=0.15))
+        b = op.spmv(np.ones(op.n))  # b = A·1 of the unscaled matrix
+        op.jacobi()  # the solve runs on D⁻¹A with D⁻¹b formed on the device
     else:
-        op = kb.Laplace3D(grid, grid, grid)
-    b = op.spmv(np.ones(op.n))  # b = A·1; the stencil is bit-identical to the reference spmv
+        if g["operator"] == "csr":
+            a = ref.laplace2d(grid, grid)
+            op = kb.CsrOperator(a.row_ptr, a.col_idx, a.vals)
+        elif dims == 2:
+            op = kb.Laplace2D(grid, grid)
+        else:
+            op = kb.Laplace3D(grid, grid, grid)
+        b = op.spmv(np.ones(op.n))  # b = A·1; the stencil is bit-identical to the reference spmv
     x0 = None if g["x0"] is None else np.full(op.n, g["x0"])
     cfg = kb.SolverConfig(scheme=kb.OrthoScheme(kb.OrthoKind(g["kind"]), g["shat"]), big_step=g["shat"],
                           max_iters=g["max_iters"])

@@ -430,7 +430,7 @@ size_t fused_fixed_smem(i64 c0) {
 bool fused_pass_supported(const StencilGeom& g, int s, i64 w, i64 c0n, i64 ld, const double* Q,
                           const double* V, const double* Vn) {
     auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    return g.dims == 2 && g.line0 == 0 && g.lines == g.ny && (g.nx & 1) == 0 && s == 5 && w == s + 1 &&
+    return g.dims == 2 && g.jacobi == 0 && g.line0 == 0 && g.lines == g.ny && (g.nx & 1) == 0 && s == 5 && w == s + 1 &&
            update_wmax(w) == 6 && c0n + w <= 64 && (ld & 1) == 0 && a16(Q) && a16(V) && a16(Vn) &&
            // the widest fused update (prefix c0n − w + 1) still gets S + 2 ring slots
            static_cast<size_t>(s + 2) * fused_slot_bytes(c0n - w + 1) + fused_fixed_smem(c0n - w + 1) <= kFuSmem &&

@@ -62,6 +62,18 @@ __device__ __forceinline__ double acc_term(double s, double coeff, double x) {
 // acc_term(s, −1, x): −1·x is exact (a sign flip), so one add of −x gives
 // the same bits.
 __device__ __forceinline__ double sub_term(double s, double x) { return __dadd_rn(s, -x); }
+// Stencil terms of A (JAC = false: off-diagonal −1, diagonal d) or of the
+// Jacobi-scaled D⁻¹A (JAC: off-diagonal c = −1/d rounded, diagonal d/d = 1),
+// each in the form spmv computes it on the (pre-scaled) CSR: the rounded
+// product, then the add (csr_matrix.hpp:75).
+template <bool JAC>
+__device__ __forceinline__ double off_term(double s, double c, double x) {
+    return JAC ? acc_term(s, c, x) : sub_term(s, x);
+}
+template <bool JAC>
+__device__ __forceinline__ double diag_term(double s, double d, double x) {
+    return JAC ? __dadd_rn(s, x) : acc_term(s, d, x);
+}
 
 constexpr int kLinesPerThread = 8;
 
@@ -71,7 +83,7 @@ constexpr int kLinesPerThread = 8;
 // plus its two (L1-resident) horizontal neighbours.  All geometry is
 // precomputed on the host (no device integer division).  Ranks own whole
 // lines (2D) / planes (3D); out-of-rank neighbours come from the halos.
-template <int DIMS, bool RESID>
+template <int DIMS, bool RESID, bool JAC>
 __global__ void __launch_bounds__(kBlock) stencil_kernel(const StencilGeom g, const double* __restrict__ x,
                                                          const double* __restrict__ halo_lo,
                                                          const double* __restrict__ halo_hi,
@@ -97,11 +109,11 @@ __global__ void __launch_bounds__(kBlock) stencil_kernel(const StencilGeom g, co
                     double up = 0.0;
                     if (has_up) up = l + 1 < g.lines ? x[i + nx] : halo_hi[ix];
                     double s = 0.0;
-                    if (gl > 0) s = acc_term(s, -1.0, down);
-                    if (ix > 0) s = acc_term(s, -1.0, x[i - 1]);
-                    s = acc_term(s, 4.0, cur);
-                    if (ix + 1 < nx) s = acc_term(s, -1.0, x[i + 1]);
-                    if (has_up) s = acc_term(s, -1.0, up);
+                    if (gl > 0) s = off_term<JAC>(s, g.c_off, down);
+                    if (ix > 0) s = off_term<JAC>(s, g.c_off, x[i - 1]);
+                    s = diag_term<JAC>(s, 4.0, cur);
+                    if (ix + 1 < nx) s = off_term<JAC>(s, g.c_off, x[i + 1]);
+                    if (has_up) s = off_term<JAC>(s, g.c_off, up);
                     if (RESID) {
                         const double r = __dsub_rn(b[i], s);
                         y[i] = r;
@@ -121,13 +133,13 @@ __global__ void __launch_bounds__(kBlock) stencil_kernel(const StencilGeom g, co
                     const i64 zl = iz - g.z0;
                     const i64 hp = iy * nx + ix;  // offset inside a halo plane
                     double s = 0.0;
-                    if (iz > 0) s = acc_term(s, -1.0, zl > 0 ? x[i - plane] : halo_lo[hp]);
-                    if (iy > 0) s = acc_term(s, -1.0, x[i - nx]);
-                    if (ix > 0) s = acc_term(s, -1.0, x[i - 1]);
-                    s = acc_term(s, 6.0, x[i]);
-                    if (ix + 1 < nx) s = acc_term(s, -1.0, x[i + 1]);
-                    if (iy + 1 < g.ny) s = acc_term(s, -1.0, x[i + nx]);
-                    if (iz + 1 < g.nz) s = acc_term(s, -1.0, zl + 1 < g.nzl ? x[i + plane] : halo_hi[hp]);
+                    if (iz > 0) s = off_term<JAC>(s, g.c_off, zl > 0 ? x[i - plane] : halo_lo[hp]);
+                    if (iy > 0) s = off_term<JAC>(s, g.c_off, x[i - nx]);
+                    if (ix > 0) s = off_term<JAC>(s, g.c_off, x[i - 1]);
+                    s = diag_term<JAC>(s, 6.0, x[i]);
+                    if (ix + 1 < nx) s = off_term<JAC>(s, g.c_off, x[i + 1]);
+                    if (iy + 1 < g.ny) s = off_term<JAC>(s, g.c_off, x[i + nx]);
+                    if (iz + 1 < g.nz) s = off_term<JAC>(s, g.c_off, zl + 1 < g.nzl ? x[i + plane] : halo_hi[hp]);
                     if (RESID) {
                         const double r = __dsub_rn(b[i], s);
                         y[i] = r;
@@ -154,7 +166,7 @@ __global__ void __launch_bounds__(kBlock) stencil_kernel(const StencilGeom g, co
 // registers, the horizontal neighbours x[i-1], x[i+2] taken from the
 // neighbouring lanes by shuffle (only lanes 0/31 touch memory for them).
 // Same per-row summation order as stencil_kernel (bit-identical).
-template <bool RESID>
+template <bool RESID, bool JAC>
 __global__ void __launch_bounds__(kBlock) stencil2d_vec_kernel(const StencilGeom g, const double* __restrict__ x,
                                                                const double* __restrict__ halo_lo,
                                                                const double* __restrict__ halo_hi,
@@ -194,16 +206,16 @@ __global__ void __launch_bounds__(kBlock) stencil2d_vec_kernel(const StencilGeom
                 if (lane == 0 && ix > 0) left = x[i - 1];
                 if (lane == 31 && ix + 2 < nx) right = x[i + 2];
                 double s0 = 0.0, s1 = 0.0;
-                if (gl > 0) s0 = sub_term(s0, down.x);
-                if (ix > 0) s0 = sub_term(s0, left);
-                s0 = acc_term(s0, 4.0, cur.x);
-                s0 = sub_term(s0, cur.y);
-                if (has_up) s0 = sub_term(s0, up.x);
-                if (gl > 0) s1 = sub_term(s1, down.y);
-                s1 = sub_term(s1, cur.x);
-                s1 = acc_term(s1, 4.0, cur.y);
-                if (ix + 2 < nx) s1 = sub_term(s1, right);
-                if (has_up) s1 = sub_term(s1, up.y);
+                if (gl > 0) s0 = off_term<JAC>(s0, g.c_off, down.x);
+                if (ix > 0) s0 = off_term<JAC>(s0, g.c_off, left);
+                s0 = diag_term<JAC>(s0, 4.0, cur.x);
+                s0 = off_term<JAC>(s0, g.c_off, cur.y);
+                if (has_up) s0 = off_term<JAC>(s0, g.c_off, up.x);
+                if (gl > 0) s1 = off_term<JAC>(s1, g.c_off, down.y);
+                s1 = off_term<JAC>(s1, g.c_off, cur.x);
+                s1 = diag_term<JAC>(s1, 4.0, cur.y);
+                if (ix + 2 < nx) s1 = off_term<JAC>(s1, g.c_off, right);
+                if (has_up) s1 = off_term<JAC>(s1, g.c_off, up.y);
                 if (RESID) {
                     const double2 bb = *reinterpret_cast<const double2*>(b + i);
                     const double r0 = __dsub_rn(bb.x, s0), r1 = __dsub_rn(bb.y, s1);
@@ -234,7 +246,7 @@ __global__ void __launch_bounds__(kBlock) stencil2d_vec_kernel(const StencilGeom
 // stencil_kernel<3> (bit-identical).
 constexpr int kPlanesPerThread = 8;
 
-template <bool RESID>
+template <bool RESID, bool JAC>
 __global__ void __launch_bounds__(kBlock, 6) stencil3d_vec_kernel(const StencilGeom g, const double* __restrict__ x,
                                                                   const double* __restrict__ halo_lo,
                                                                   const double* __restrict__ halo_hi,
@@ -278,20 +290,20 @@ __global__ void __launch_bounds__(kBlock, 6) stencil3d_vec_kernel(const StencilG
                 const double2 ym = has_ym ? ld2(xc - nx) : make_double2(0.0, 0.0);
                 const double2 yp = has_yp ? ld2(xc + nx) : make_double2(0.0, 0.0);
                 double s0 = 0.0, s1 = 0.0;
-                if (has_dn) s0 = sub_term(s0, down.x);
-                if (has_ym) s0 = sub_term(s0, ym.x);
-                if (has_l) s0 = sub_term(s0, left);
-                s0 = acc_term(s0, 6.0, cur.x);
-                s0 = sub_term(s0, cur.y);
-                if (has_yp) s0 = sub_term(s0, yp.x);
-                if (has_up) s0 = sub_term(s0, up.x);
-                if (has_dn) s1 = sub_term(s1, down.y);
-                if (has_ym) s1 = sub_term(s1, ym.y);
-                s1 = sub_term(s1, cur.x);
-                s1 = acc_term(s1, 6.0, cur.y);
-                if (has_r) s1 = sub_term(s1, right);
-                if (has_yp) s1 = sub_term(s1, yp.y);
-                if (has_up) s1 = sub_term(s1, up.y);
+                if (has_dn) s0 = off_term<JAC>(s0, g.c_off, down.x);
+                if (has_ym) s0 = off_term<JAC>(s0, g.c_off, ym.x);
+                if (has_l) s0 = off_term<JAC>(s0, g.c_off, left);
+                s0 = diag_term<JAC>(s0, 6.0, cur.x);
+                s0 = off_term<JAC>(s0, g.c_off, cur.y);
+                if (has_yp) s0 = off_term<JAC>(s0, g.c_off, yp.x);
+                if (has_up) s0 = off_term<JAC>(s0, g.c_off, up.x);
+                if (has_dn) s1 = off_term<JAC>(s1, g.c_off, down.y);
+                if (has_ym) s1 = off_term<JAC>(s1, g.c_off, ym.y);
+                s1 = off_term<JAC>(s1, g.c_off, cur.x);
+                s1 = diag_term<JAC>(s1, 6.0, cur.y);
+                if (has_r) s1 = off_term<JAC>(s1, g.c_off, right);
+                if (has_yp) s1 = off_term<JAC>(s1, g.c_off, yp.y);
+                if (has_up) s1 = off_term<JAC>(s1, g.c_off, up.y);
                 if (RESID) {
                     const double2 bb = ld2(bc);
                     bc += plane;
@@ -339,7 +351,7 @@ __global__ void __launch_bounds__(kBlock, 6) stencil3d_vec_kernel(const StencilG
 // same result as skipping the term.
 constexpr int kMpkRing = 3;
 
-template <int S>
+template <int S, bool JAC>
 __device__ __forceinline__ void mpk2d_task(const StencilGeom& g, const double* __restrict__ x,
                                            const double* __restrict__ halo_lo, const double* __restrict__ halo_hi,
                                            double* __restrict__ out, i64 ldo, int wb, int wx, int band, int lane) {
@@ -400,16 +412,16 @@ __device__ __forceinline__ void mpk2d_task(const StencilGeom& g, const double* _
             const double2 up = k == 1 ? in : r[P1][k - 1];
             const double left = __shfl_up_sync(0xffffffffu, cu.y, 1);
             const double right = __shfl_down_sync(0xffffffffu, cu.x, 1);
-            double s0 = __dadd_rn(0.0, -dn.x);
-            s0 = __dadd_rn(s0, -left);
-            s0 = acc_term(s0, 4.0, cu.x);
-            s0 = __dadd_rn(s0, -cu.y);
-            s0 = __dadd_rn(s0, -up.x);
-            double s1 = __dadd_rn(0.0, -dn.y);
-            s1 = __dadd_rn(s1, -cu.x);
-            s1 = acc_term(s1, 4.0, cu.y);
-            s1 = __dadd_rn(s1, -right);
-            s1 = __dadd_rn(s1, -up.y);
+            double s0 = off_term<JAC>(0.0, g.c_off, dn.x);
+            s0 = off_term<JAC>(s0, g.c_off, left);
+            s0 = diag_term<JAC>(s0, 4.0, cu.x);
+            s0 = off_term<JAC>(s0, g.c_off, cu.y);
+            s0 = off_term<JAC>(s0, g.c_off, up.x);
+            double s1 = off_term<JAC>(0.0, g.c_off, dn.y);
+            s1 = off_term<JAC>(s1, g.c_off, cu.x);
+            s1 = diag_term<JAC>(s1, 4.0, cu.y);
+            s1 = off_term<JAC>(s1, g.c_off, right);
+            s1 = off_term<JAC>(s1, g.c_off, up.y);
             // outside the grid (lines or columns): exactly +0.0
             const bool live = in_grid && (FAST || (gl >= 0 && gl < ny));
             const double2 v = live ? make_double2(s0, s1) : make_double2(0.0, 0.0);
@@ -434,7 +446,7 @@ __device__ __forceinline__ void mpk2d_task(const StencilGeom& g, const double* _
     }
 }
 
-template <int S>
+template <int S, bool JAC>
 __global__ void __launch_bounds__(kBlock, 2) mpk2d_kernel(const StencilGeom g, const double* __restrict__ x,
                                                        const double* __restrict__ halo_lo,
                                                        const double* __restrict__ halo_hi,
@@ -445,9 +457,128 @@ __global__ void __launch_bounds__(kBlock, 2) mpk2d_kernel(const StencilGeom g, c
     const i64 nwarps = static_cast<i64>(gridDim.x) * (kBlock / 32);
     for (i64 task = blockIdx.x * static_cast<i64>(kBlock / 32) + (threadIdx.x >> 5); task < ntasks;
          task += nwarps)  // whole warps only
-        mpk2d_task<S>(g, x, halo_lo, halo_hi, out, ldo, static_cast<int>(task / nwx), static_cast<int>(task % nwx),
+        mpk2d_task<S, JAC>(g, x, halo_lo, halo_hi, out, ldo, static_cast<int>(task / nwx), static_cast<int>(task % nwx),
                       static_cast<int>(band), lane);
 }
+
+// K2g: the whole s-step MPK of the 7-point stencil in one pass
+// (mpk_monomial, gmres.hpp:80-90, on gen_laplace3d, matgen.hpp:167-187):
+// out[:, k−1] = A^k·x for k = 1..S.  Temporal blocking along z: a CTA of
+// 32 warps owns a 64 × 32 (x × y) tile of grid columns — warp w is tile row
+// w, lane l holds columns 2l, 2l+1 as a double2 — and a band of z-planes,
+// and streams the band's input planes once, bottom to top.  Level k runs k
+// planes behind the input (at step t it produces plane zs + t − k), all S
+// levels of a step computed bottom-up, so level k's upper neighbour (level
+// k − 1, plane + 1) was produced earlier in the same step and its own
+// column's lower/current planes sit in a two-deep register history.  The
+// in-plane neighbours: x by shuffle, y from the tile row above/below, which
+// every level publishes in a shared-memory plane double-buffered by step
+// parity (read slot t−1, write slot t, one __syncthreads per step) —
+// 2·S·16 KB.  Level k is valid on the tile shrunk by k cells per side (x by
+// H = S rounded up to even, for the double2 columns), so a tile outputs its
+// middle (64 − 2H) × (32 − 2S) columns and neighbouring tiles overlap; the
+// band starts S planes early (recomputed, never stored).  HBM traffic: one
+// read of x (+ the overlaps, mostly L2) and S writes, against S reads and S
+// writes for S separate SpMVs.  Bit-identity with spmv: every element is
+// 0.0 + t_0 + … + t_6 in stored column order (z−1, y−1, x−1, centre, x+1,
+// y+1, z+1), absent neighbours carried as +0.0 and added as −0.0 (see K2f).
+// JAC: the Jacobi-scaled operator D⁻¹A of gen_laplace3d (off-diagonal
+// coefficient g.c_off = −1/6 rounded, centre 6/6 = 1; off_term/diag_term).
+constexpr int kMpk3Warps = 32;
+
+template <int S, bool JAC>
+__global__ void __launch_bounds__(kMpk3Warps * 32, 1)
+    mpk3d_kernel(const StencilGeom g, const double* __restrict__ x, const double* __restrict__ halo_lo,
+                 const double* __restrict__ halo_hi, double* __restrict__ out, i64 ldo, int nwx, int nwy,
+                 int band, int ntasks) {
+    KB_PDL_WAIT();
+    constexpr int H = (S + 1) & ~1;
+    constexpr int STEPX = 64 - 2 * H;
+    constexpr int STEPY = kMpk3Warps - 2 * S;
+    constexpr int ROW = 32;  // double2 per tile row
+    constexpr int PLANE = kMpk3Warps * ROW;  // double2 per tile plane
+    extern __shared__ double2 sm3[];  // [2 slots][S levels][32 rows][32 lanes]
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int nx = static_cast<int>(g.nx), ny = static_cast<int>(g.ny), nz = static_cast<int>(g.nz);
+    const int nzl = static_cast<int>(g.nzl), z0 = static_cast<int>(g.z0);
+    const i64 nx64 = nx, plane = static_cast<i64>(nx) * ny;
+    for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
+        const int wx = task % nwx, wy = (task / nwx) % nwy, wz = task / (nwx * nwy);
+        const int ix = wx * STEPX - H + 2 * lane, iy = wy * STEPY - S + w;
+        const bool in_plane = ix >= 0 && ix < nx && iy >= 0 && iy < ny;  // nx even: both columns or neither
+        const bool store_cell = in_plane && lane >= H / 2 && lane < 32 - H / 2 && w >= S && w < kMpk3Warps - S;
+        const int zb0 = wz * band, zb1 = min(zb0 + band, nzl);
+        const int zs = max(zb0 - S, -z0);             // first input plane (local index)
+        const int zmax = min(nzl + S, nz - z0);       // first plane with no data (zeros above)
+        const int steps = zb1 - zs + S;
+        const i64 cell = static_cast<i64>(iy) * nx64 + ix;
+        auto load = [&](int l) -> double2 {
+            double2 v = make_double2(0.0, 0.0);
+            if (in_plane && l < zmax) {
+                const double* p = l < 0       ? halo_lo + static_cast<i64>(l + S) * plane
+                                  : l < nzl ? x + static_cast<i64>(l) * plane
+                                            : halo_hi + static_cast<i64>(l - nzl) * plane;
+                v = __ldg(reinterpret_cast<const double2*>(p + cell));
+            }
+            return v;
+        };
+        // h2[j]: level j's column at the plane of step t − 2 (the step t − 1
+        // plane is read back from the shared slot, with the y-neighbours).
+        double2 h2[S];
+#pragma unroll
+        for (int j = 0; j < S; ++j) h2[j] = make_double2(0.0, 0.0);
+        double2 pf0 = load(zs), pf1 = load(zs + 1);
+        __syncthreads();  // the previous task's last reads of the shared planes are done
+        // the "step −1" planes (slot 1): +0.0, what lies below the grid's first plane
+#pragma unroll
+        for (int j = 0; j < S; ++j) sm3[(1 * S + j) * PLANE + w * ROW + lane] = make_double2(0.0, 0.0);
+        __syncthreads();
+        for (int t = 0; t < steps; ++t) {
+            const int cur = t & 1, prv = cur ^ 1;
+            double2 up = pf0;  // level 0 (the input) at plane zs + t
+            pf0 = pf1;
+            pf1 = load(zs + t + 2);
+            sm3[(cur * S + 0) * PLANE + w * ROW + lane] = up;
+#pragma unroll
+            for (int k = 1; k <= S; ++k) {
+                const int l = zs + t - k;  // level k's plane this step
+                const int gz = z0 + l;
+                const double2* pl = sm3 + (prv * S + (k - 1)) * PLANE + w * ROW + lane;
+                const double2 cu = pl[0];
+                const double2 ym = w > 0 ? pl[-ROW] : make_double2(0.0, 0.0);
+                const double2 yp = w + 1 < kMpk3Warps ? pl[ROW] : make_double2(0.0, 0.0);
+                const double2 dn = h2[k - 1];
+                h2[k - 1] = cu;
+                const double left = __shfl_up_sync(0xffffffffu, cu.y, 1);
+                const double right = __shfl_down_sync(0xffffffffu, cu.x, 1);
+                double s0 = off_term<JAC>(0.0, g.c_off, dn.x);
+                s0 = off_term<JAC>(s0, g.c_off, ym.x);
+                s0 = off_term<JAC>(s0, g.c_off, left);
+                s0 = diag_term<JAC>(s0, 6.0, cu.x);
+                s0 = off_term<JAC>(s0, g.c_off, cu.y);
+                s0 = off_term<JAC>(s0, g.c_off, yp.x);
+                s0 = off_term<JAC>(s0, g.c_off, up.x);
+                double s1 = off_term<JAC>(0.0, g.c_off, dn.y);
+                s1 = off_term<JAC>(s1, g.c_off, ym.y);
+                s1 = off_term<JAC>(s1, g.c_off, cu.x);
+                s1 = diag_term<JAC>(s1, 6.0, cu.y);
+                s1 = off_term<JAC>(s1, g.c_off, right);
+                s1 = off_term<JAC>(s1, g.c_off, yp.y);
+                s1 = off_term<JAC>(s1, g.c_off, up.y);
+                // outside the grid: exactly +0.0 (an absent neighbour of a valid cell)
+                const bool live = in_plane && gz >= 0 && gz < nz;
+                const double2 v = live ? make_double2(s0, s1) : make_double2(0.0, 0.0);
+                if (store_cell && l >= zb0 && l < zb1)
+                    *reinterpret_cast<double2*>(out + static_cast<i64>(k - 1) * ldo + static_cast<i64>(l) * plane +
+                                                cell) = v;
+                if (k < S) sm3[(cur * S + k) * PLANE + w * ROW + lane] = v;
+                up = v;  // level k at plane l is level k + 1's upper neighbour
+            }
+            __syncthreads();
+        }
+    }
+}
+
 
 // CSR SpMV, one warp per 32 consecutive rows, in two phases per chunk of
 // the warp's contiguous nnz range (kCsrChunk entries):
@@ -583,6 +714,8 @@ StencilGeom make_stencil_geom(int dims, i64 nx, i64 ny, i64 nz, i64 row_begin, i
     g.line0 = row_begin / nx;
     g.z0 = dims == 2 ? 0 : row_begin / (nx * ny);
     g.nzl = dims == 2 ? 0 : nloc / (nx * ny);
+    g.jacobi = 0;
+    g.c_off = -1.0;
     return g;
 }
 
@@ -604,9 +737,9 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
         dim3 grid = stencil_grid(g);
         grid.x = static_cast<unsigned>(ceil_div(g.nx / 2, kBlock));
         if (b)
-            launch_pdl(stencil2d_vec_kernel<true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
+            (g.jacobi ? launch_pdl(stencil2d_vec_kernel<true, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials) : launch_pdl(stencil2d_vec_kernel<true, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials));
         else
-            launch_pdl(stencil2d_vec_kernel<false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
+            (g.jacobi ? launch_pdl(stencil2d_vec_kernel<false, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials) : launch_pdl(stencil2d_vec_kernel<false, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials));
         KB_LAUNCHED();
         ++launches;
         return b ? static_cast<int>(grid.x * grid.y) : 0;
@@ -618,9 +751,9 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
     if (vec3 && g.dims == 3 && (g.nx & 1) == 0 && g.nx * g.ny < (i64(1) << 30) && g.nzl < (i64(1) << 30) && a16(x) && a16(y) && a16(b) && a16(halo_lo) && a16(halo_hi)) {
         const dim3 grid = stencil3d_vec_grid(g);
         if (b)
-            launch_pdl(stencil3d_vec_kernel<true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
+            (g.jacobi ? launch_pdl(stencil3d_vec_kernel<true, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials) : launch_pdl(stencil3d_vec_kernel<true, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials));
         else
-            launch_pdl(stencil3d_vec_kernel<false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
+            (g.jacobi ? launch_pdl(stencil3d_vec_kernel<false, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials) : launch_pdl(stencil3d_vec_kernel<false, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials));
         KB_LAUNCHED();
         ++launches;
         return b ? static_cast<int>(grid.x * grid.y) : 0;
@@ -628,14 +761,14 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
     const dim3 grid = stencil_grid(g);
     if (g.dims == 2) {
         if (b)
-            launch_pdl(stencil_kernel<2, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
+            (g.jacobi ? launch_pdl(stencil_kernel<2, true, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials) : launch_pdl(stencil_kernel<2, true, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials));
         else
-            launch_pdl(stencil_kernel<2, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
+            (g.jacobi ? launch_pdl(stencil_kernel<2, false, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials) : launch_pdl(stencil_kernel<2, false, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials));
     } else {
         if (b)
-            launch_pdl(stencil_kernel<3, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
+            (g.jacobi ? launch_pdl(stencil_kernel<3, true, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials) : launch_pdl(stencil_kernel<3, true, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials));
         else
-            launch_pdl(stencil_kernel<3, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials);
+            (g.jacobi ? launch_pdl(stencil_kernel<3, false, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials) : launch_pdl(stencil_kernel<3, false, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials));
     }
     KB_LAUNCHED();
     ++launches;
@@ -700,16 +833,75 @@ void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const 
         launch_pdl(kernel, grid, kBlock, 0, st, g, x, halo_lo, halo_hi, out, ldo, nwx, band, ntasks);
     };
     switch (s) {
-        case 1: go(mpk2d_kernel<1>); break;
-        case 2: go(mpk2d_kernel<2>); break;
-        case 3: go(mpk2d_kernel<3>); break;
-        case 4: go(mpk2d_kernel<4>); break;
-        case 5: go(mpk2d_kernel<5>); break;
-        case 6: go(mpk2d_kernel<6>); break;
-        case 7: go(mpk2d_kernel<7>); break;
-        case 8: go(mpk2d_kernel<8>); break;
+        case 1: g.jacobi ? go(mpk2d_kernel<1, true>) : go(mpk2d_kernel<1, false>); break;
+        case 2: g.jacobi ? go(mpk2d_kernel<2, true>) : go(mpk2d_kernel<2, false>); break;
+        case 3: g.jacobi ? go(mpk2d_kernel<3, true>) : go(mpk2d_kernel<3, false>); break;
+        case 4: g.jacobi ? go(mpk2d_kernel<4, true>) : go(mpk2d_kernel<4, false>); break;
+        case 5: g.jacobi ? go(mpk2d_kernel<5, true>) : go(mpk2d_kernel<5, false>); break;
+        case 6: g.jacobi ? go(mpk2d_kernel<6, true>) : go(mpk2d_kernel<6, false>); break;
+        case 7: g.jacobi ? go(mpk2d_kernel<7, true>) : go(mpk2d_kernel<7, false>); break;
+        case 8: g.jacobi ? go(mpk2d_kernel<8, true>) : go(mpk2d_kernel<8, false>); break;
         default: fail(KRY_INTERNAL, "mpk2d: unsupported s");
     }
+    KB_LAUNCHED();
+    ++launches;
+}
+
+bool mpk3d_supported(const StencilGeom& g, int s, const double* x, const double* out, i64 ldo, bool force) {
+    auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
+    if (!(g.dims == 3 && (g.nx & 1) == 0 && s >= 1 && s <= 7 && (ldo & 1) == 0 && a16(x) && a16(out) &&
+          g.nzl >= 1 && g.nx + 64 < (i64(1) << 31) && g.ny + 64 < (i64(1) << 31) && g.nz + 16 < (i64(1) << 31)))
+        return false;
+    // Worth it once the (tile, band) tasks fill the GPU with one CTA per SM.
+    const int h = (s + 1) & ~1;
+    const i64 tiles = ceil_div(g.nx, 64 - 2 * h) * ceil_div(g.ny, kMpk3Warps - 2 * s);
+    const i64 tasks = tiles * std::max<i64>(1, g.nzl / (4 * s));
+    return force || tasks >= static_cast<i64>(num_sms());
+}
+
+void launch_mpk3d(cudaStream_t st, const StencilGeom& g, const double* x, const double* halo_lo,
+                  const double* halo_hi, double* out, i64 ldo, int s, int64_t& launches) {
+    const bool jacobi = g.jacobi != 0;
+    const int h = (s + 1) & ~1;
+    const i64 nwx = ceil_div(g.nx, 64 - 2 * h), nwy = ceil_div(g.ny, kMpk3Warps - 2 * s);
+    const i64 sms = num_sms();
+    // z-bands per tile: minimise rounds × (band + 2s) steps per CTA (one CTA per SM)
+    i64 nzb = 1, best = -1;
+    for (i64 b = 1; b <= std::max<i64>(1, g.nzl / s) && b <= 4096; ++b) {
+        const i64 tasks = nwx * nwy * b, rounds = ceil_div(tasks, sms);
+        const i64 cost = rounds * (ceil_div(g.nzl, b) + 2 * s);
+        if (best < 0 || cost < best) {
+            best = cost;
+            nzb = b;
+        }
+    }
+    const i64 band = ceil_div(g.nzl, nzb);
+    nzb = ceil_div(g.nzl, band);
+    const i64 ntasks = nwx * nwy * nzb;
+    if (ntasks >= (i64(1) << 31)) fail(KRY_UNSUPPORTED, "mpk3d: too many tiles");
+    const size_t smem = static_cast<size_t>(2 * s) * kMpk3Warps * 32 * sizeof(double2);
+    const unsigned grid = static_cast<unsigned>(std::min<i64>(ntasks, sms));
+    auto go = [&](auto kernel) {
+        set_kernel_smem(reinterpret_cast<const void*>(kernel), smem);
+        launch_pdl(kernel, grid, kMpk3Warps * 32, smem, st, g, x, halo_lo, halo_hi, out, ldo, static_cast<int>(nwx),
+                   static_cast<int>(nwy), static_cast<int>(band), static_cast<int>(ntasks));
+    };
+#define KB_MPK3(SV)                                           \
+    case SV:                                                  \
+        if (jacobi) go(mpk3d_kernel<SV, true>);               \
+        else go(mpk3d_kernel<SV, false>);                     \
+        break;
+    switch (s) {
+        KB_MPK3(1)
+        KB_MPK3(2)
+        KB_MPK3(3)
+        KB_MPK3(4)
+        KB_MPK3(5)
+        KB_MPK3(6)
+        KB_MPK3(7)
+        default: fail(KRY_INTERNAL, "mpk3d: unsupported s");
+    }
+#undef KB_MPK3
     KB_LAUNCHED();
     ++launches;
 }

@@ -73,6 +73,10 @@ struct StencilGeom {
     i64 line0;       // global index of the first owned line
     i64 z0;          // first owned plane (3D)
     i64 nzl;         // owned planes (3D)
+    // Jacobi-scaled operator D⁻¹A (kry_operator_jacobi): off-diagonal
+    // coefficient c_off = −1/diag (rounded), diagonal 1; else −1 / diag.
+    int jacobi;
+    double c_off;
 };
 StencilGeom make_stencil_geom(int dims, i64 nx, i64 ny, i64 nz, i64 row_begin, i64 nloc);
 // y = A·x (b == nullptr) or r = b − A·x with Σr² partials (b != nullptr);
@@ -85,6 +89,11 @@ int stencil_partials(const StencilGeom& g);
 // force: skip the size heuristic (tests).
 bool mpk2d_supported(const StencilGeom& g, int s, const double* x, const double* out, i64 ldo, bool force);
 void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const double* halo_lo,
+                  const double* halo_hi, double* out, i64 ldo, int s, int64_t& launches);
+// Fused 3-D MPK (7-point stencil, temporal blocking along z): out[:, k−1] =
+// A^k·x (or (D⁻¹A)^k·x with jacobi), k = 1..s ≤ 7; halos hold s planes each.
+bool mpk3d_supported(const StencilGeom& g, int s, const double* x, const double* out, i64 ldo, bool force);
+void launch_mpk3d(cudaStream_t st, const StencilGeom& g, const double* x, const double* halo_lo,
                   const double* halo_hi, double* out, i64 ldo, int s, int64_t& launches);
 // CSR rows (row_ptr local, from 0) gathering x through int32 indices.
 int launch_csr(cudaStream_t s, i64 nloc, const int64_t* row_ptr, const int32_t* col, const double* vals,

@@ -235,19 +235,26 @@ bool Operator::mpk(const double* x, double* out, i64 ldo, int s) {
     const char* e = std::getenv("KRY_FUSED_MPK");
     const int mode = e ? std::atoi(e) : 1;
     Ctx& c = *ctx;
-    // Every rank must own at least s lines (the halo is the neighbour's s
-    // edge lines); the partition differs by at most one line between ranks.
-    // The choice pairs every rank's sends with its neighbours' receives, so
-    // it must be the same on every rank: the size heuristic is judged on the
-    // smallest rank's line count (ny / nranks, known to all ranks), not on
-    // this rank's own.  The other inputs (s, nx, the store's even ld, 256-byte
-    // aligned allocations) are identical on every rank.
+    if (mode == 0 || kind == CSR) return false;
+    // Every rank must own at least s lines / planes (the halo is the
+    // neighbour's s edge lines / planes); the partition differs by at most
+    // one line / plane between ranks.  The choice pairs every rank's sends
+    // with its neighbours' receives, so it must be the same on every rank:
+    // the size heuristic is judged on the smallest rank's share (known to
+    // all ranks), not on this rank's own.  The other inputs (s, the grid,
+    // the store's even ld, 256-byte aligned allocations) are identical on
+    // every rank.
     StencilGeom uniform = geom;
-    uniform.lines = geom.ny / c.nranks;
-    if (mode == 0 || kind != LAPLACE2D || uniform.lines < s ||
-        !mpk2d_supported(uniform, s, x, out, ldo, mode == 2))
-        return false;
-    const i64 h = static_cast<i64>(s) * geom.nx;
+    i64 plane = geom.nx;
+    if (kind == LAPLACE2D) {
+        uniform.lines = geom.ny / c.nranks;
+        if (uniform.lines < s || !mpk2d_supported(uniform, s, x, out, ldo, mode == 2)) return false;
+    } else {
+        uniform.nzl = geom.nz / c.nranks;
+        plane = geom.nx * geom.ny;
+        if (uniform.nzl < s || !mpk3d_supported(uniform, s, x, out, ldo, mode == 2)) return false;
+    }
+    const i64 h = static_cast<i64>(s) * plane;
     if (c.nranks > 1) {
         mpk_lo.ensure(static_cast<size_t>(h) * 8);
         mpk_hi.ensure(static_cast<size_t>(h) * 8);
@@ -262,15 +269,26 @@ bool Operator::mpk(const double* x, double* out, i64 ldo, int s) {
         }
         KB_NCCL(ncclGroupEnd());
     }
-    launch_mpk2d(c.stream, geom, x, mpk_lo.p, mpk_hi.p, out, ldo, s, c.launches);
+    if (kind == LAPLACE2D)
+        launch_mpk2d(c.stream, geom, x, mpk_lo.p, mpk_hi.p, out, ldo, s, c.launches);
+    else
+        launch_mpk3d(c.stream, geom, x, mpk_lo.p, mpk_hi.p, out, ldo, s, c.launches);
     return true;
 }
 
 void Operator::set_jacobi() {
     if (jacobi) return;
     Ctx& c = *ctx;
-    if (kind != CSR)
-        fail(KRY_UNSUPPORTED, "Jacobi scaling is implemented for CSR operators (the Laplacians' diagonal is constant)");
+    if (kind != CSR) {
+        // gen_laplace2d/3d: every row's diagonal is 4 / 6, so D⁻¹A is the
+        // stencil with off-diagonal −1/d (rounded, as a_ij / a_ii is) and
+        // diagonal 1 — applied inside the stencil and MPK kernels.
+        const double d = kind == LAPLACE2D ? 4.0 : 6.0;
+        geom.jacobi = 1;
+        geom.c_off = -1.0 / d;
+        jacobi = true;
+        return;
+    }
     diag.ensure(static_cast<size_t>(std::max<i64>(nloc, 1)) * 8);
     KB_CUDA(cudaMemsetAsync(diag.p, 0, static_cast<size_t>(std::max<i64>(nloc, 1)) * 8, c.stream));
     // the diagonal of local row i is gathered column (rank·max_rows + i)
@@ -306,7 +324,10 @@ void Operator::set_jacobi() {
 const double* Operator::scaled_rhs(const double* b, DevBuf& buf) {
     if (!jacobi) return b;
     buf.ensure(static_cast<size_t>(std::max<i64>(nloc, 1)) * 8);
-    launch_div_diag(ctx->stream, nloc, b, diag.p, 0.0, buf.p, ctx->launches);
+    if (kind == CSR)
+        launch_div_diag(ctx->stream, nloc, b, diag.p, 0.0, buf.p, ctx->launches);
+    else
+        launch_div_diag(ctx->stream, nloc, b, nullptr, kind == LAPLACE2D ? 4.0 : 6.0, buf.p, ctx->launches);
     return buf.p;
 }
 

@@ -87,7 +87,9 @@ def main():
     for name, a, mk, s in [("mpk_2d100_s5", ref.laplace2d(100, 100), lambda: kb.Laplace2D(100, 100, ctx), 5),
                            ("mpk_2d96_s8", ref.laplace2d(96, 64), lambda: kb.Laplace2D(96, 64, ctx), 8),
                            ("mpk_2d101_s5", ref.laplace2d(101, 40), lambda: kb.Laplace2D(101, 40, ctx), 5),
-                           ("mpk_3d12_s5", ref.laplace3d(12, 12, 12), lambda: kb.Laplace3D(12, 12, 12, ctx), 5)]:
+                           ("mpk_3d12_s5", ref.laplace3d(12, 12, 12), lambda: kb.Laplace3D(12, 12, 12, ctx), 5),
+                           ("mpk_3d70x40x31_s5", ref.laplace3d(70, 40, 31),
+                            lambda: kb.Laplace3D(70, 40, 31, ctx), 5)]:
         op = mk()
         start = rng.standard_normal(a.n)
         start /= np.linalg.norm(start)

@@ -116,6 +116,65 @@ def test_mpk_fused_bitwise(kb, ctx, ref, rng, monkeypatch, nx, ny, s):
     np.testing.assert_array_equal(op.mpk(start, s), ref.mpk(a, start, s))
 
 
+# The fused 3-D MPK (k_ops.cu mpk3d_kernel: temporal blocking along z,
+# 64 × 32 tiles shrinking by the level): tile seams in x (nx > 52) and y
+# (ny > 22), z-band seams, odd nx (per-SpMV fallback), s up to 7 (s = 8
+# falls back), grids smaller than one tile.
+@pytest.mark.parametrize("nx,ny,nz,s", [(64, 64, 64, 5), (130, 50, 20, 5), (200, 40, 33, 7), (52, 33, 100, 5),
+                                        (2, 2, 2, 1), (8, 300, 7, 3), (106, 23, 41, 2), (58, 45, 12, 6),
+                                        (131, 20, 10, 5), (64, 64, 9, 8), (110, 22, 60, 4), (256, 256, 17, 5)])
+def test_mpk3d_fused_bitwise(kb, ctx, ref, rng, monkeypatch, nx, ny, nz, s):
+    monkeypatch.setenv("KRY_FUSED_MPK", "2")  # below the size heuristic: force the fused kernel
+    a = ref.laplace3d(nx, ny, nz)
+    op = kb.Laplace3D(nx, ny, nz)
+    start = rng.standard_normal(a.n)
+    start /= np.linalg.norm(start)
+    np.testing.assert_array_equal(op.mpk(start, s), ref.mpk(a, start, s))
+
+
+def prescaled(a):
+    """D⁻¹A of a reference CSR on the host: a_ij / a_ii row by row."""
+    from oracle import ref as R
+    rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+    d = a.vals[a.col_idx == rows]
+    return R.Csr(a.n, a.row_ptr, a.col_idx, a.vals / d[rows])
+
+
+@pytest.mark.parametrize("dims,shape,fused", [(2, (130, 97), "2"), (2, (131, 50), "2"), (2, (40, 30), "0"),
+                                              (3, (58, 45, 12), "2"), (3, (17, 9, 11), "0"),
+                                              (3, (64, 64, 64), "0")])
+def test_jacobi_stencil_bitwise(kb, ctx, ref, rng, monkeypatch, dims, shape, fused):
+    """Jacobi on the matrix-free Laplacians: the stencil and MPK kernels apply
+    D⁻¹A (off-diagonal −1/d rounded, diagonal 1) bit-identically to the
+    reference's spmv / mpk_monomial on the host pre-scaled CSR."""
+    monkeypatch.setenv("KRY_FUSED_MPK", fused)
+    a = ref.laplace2d(*shape) if dims == 2 else ref.laplace3d(*shape)
+    op = (kb.Laplace2D if dims == 2 else kb.Laplace3D)(*shape)
+    op.jacobi()
+    assert op.is_jacobi
+    aj = prescaled(a)
+    x = rng.standard_normal(a.n)
+    np.testing.assert_array_equal(op.spmv(x), ref.spmv(aj, x))
+    np.testing.assert_array_equal(op.mpk(x, 5), ref.mpk(aj, x, 5))
+
+
+@pytest.mark.parametrize("dims,g,kind,shat", [(2, 64, 3, 60), (2, 100, 2, 0), (3, 16, 3, 60), (3, 24, 3, 20)])
+def test_jacobi_stencil_solve_matches_reference(kb, ctx, ref, dims, g, kind, shat):
+    """A Jacobi-preconditioned solve: the reference is handed D⁻¹A and D⁻¹b
+    (b = A·1), the device gets A, b and kry_operator_jacobi."""
+    a = ref.laplace2d(g, g) if dims == 2 else ref.laplace3d(g, g, g)
+    b = ref.spmv(a, np.ones(a.n))
+    want = ref.solve(prescaled(a), b / (4.0 if dims == 2 else 6.0), None,
+                     ref.make_config(kind=kind, big_step=shat, shat=shat))
+    op = (kb.Laplace2D(g, g) if dims == 2 else kb.Laplace3D(g, g, g)).jacobi()
+    got = kb.sstep_gmres(op, b, None, kb.SolverConfig(scheme=kb.OrthoScheme(kb.OrthoKind(kind), shat),
+                                                     big_step=shat))
+    assert (int(got.status), got.iterations, got.restarts, got.sync.reduces) == (
+        want.status, want.iterations, want.restarts, want.reduces)
+    assert abs(got.cycle_residuals[0] - want.cycle_residuals[0]) <= 1e-10 * want.cycle_residuals[0] + 1e-13
+    assert abs(got.initial_residual - want.initial_residual) <= 1e-12 * want.initial_residual
+
+
 def test_spmv_rejects_bad_length(kb, ctx):
     op = kb.Laplace2D(4, 4)
     with pytest.raises(kb.DimensionMismatch):

@@ -464,27 +464,31 @@ __global__ void __launch_bounds__(kBlock, 2) mpk2d_kernel(const StencilGeom g, c
 // K2g: the whole s-step MPK of the 7-point stencil in one pass
 // (mpk_monomial, gmres.hpp:80-90, on gen_laplace3d, matgen.hpp:167-187):
 // out[:, k−1] = A^k·x for k = 1..S.  Temporal blocking along z: a CTA of
-// 32 warps owns a 64 × 32 (x × y) tile of grid columns — warp w is tile row
-// w, lane l holds columns 2l, 2l+1 as a double2 — and a band of z-planes,
-// and streams the band's input planes once, bottom to top.  Level k runs k
-// planes behind the input (at step t it produces plane zs + t − k), all S
-// levels of a step computed bottom-up, so level k's upper neighbour (level
-// k − 1, plane + 1) was produced earlier in the same step and its own
-// column's lower/current planes sit in a two-deep register history.  The
-// in-plane neighbours: x by shuffle, y from the tile row above/below, which
-// every level publishes in a shared-memory plane double-buffered by step
-// parity (read slot t−1, write slot t, one __syncthreads per step) —
-// 2·S·16 KB.  Level k is valid on the tile shrunk by k cells per side (x by
-// H = S rounded up to even, for the double2 columns), so a tile outputs its
-// middle (64 − 2H) × (32 − 2S) columns and neighbouring tiles overlap; the
-// band starts S planes early (recomputed, never stored).  HBM traffic: one
-// read of x (+ the overlaps, mostly L2) and S writes, against S reads and S
-// writes for S separate SpMVs.  Bit-identity with spmv: every element is
-// 0.0 + t_0 + … + t_6 in stored column order (z−1, y−1, x−1, centre, x+1,
-// y+1, z+1), absent neighbours carried as +0.0 and added as −0.0 (see K2f).
-// JAC: the Jacobi-scaled operator D⁻¹A of gen_laplace3d (off-diagonal
-// coefficient g.c_off = −1/6 rounded, centre 6/6 = 1; off_term/diag_term).
-constexpr int kMpk3Warps = 32;
+// 16 warps owns a 64 × 32 (x × y) tile of grid columns — warp w holds tile
+// rows 2w and 2w + 1, lane l columns 2l and 2l + 1 of both (two double2) —
+// and a band of z-planes, and streams the band's input planes once, bottom
+// to top.  Level k runs k planes behind the input (at step t it produces
+// plane zs + t − k); the S levels of a step are computed bottom-up, so level
+// k's upper neighbour (level k − 1, plane + 1) was produced earlier in the
+// same step; a thread's own columns one plane below sit in registers, two
+// planes below in its own cells of the shared slot.  In-plane neighbours: x by shuffle;
+// y from the thread's other row, or — for the rows the next warps own —
+// from a shared-memory copy of each level's plane, double-buffered by step
+// parity (read slot t − 1, write slot t, one __syncthreads per step; rows
+// −1 and 32 are zero padding).  Level k is valid on the tile shrunk by k
+// cells per side (x by H = S rounded up to even, for the double2 columns),
+// so a tile outputs its middle (64 − 2H) × (32 − 2S) columns and
+// neighbouring tiles overlap; the band starts S planes early (recomputed,
+// never stored).  HBM traffic: one read of x (+ the overlaps, mostly L2)
+// and S writes, against S reads and S writes for S separate SpMVs.
+// Bit-identity with spmv: every element is 0.0 + t_0 + … + t_6 in stored
+// column order (z−1, y−1, x−1, centre, x+1, y+1, z+1); absent neighbours
+// are carried as +0.0 and added as −0.0 (see K2f).  Interior tiles and
+// steps (warp-uniform) skip the grid-edge masks.  JAC: the Jacobi-scaled
+// operator D⁻¹A (off_term / diag_term).
+constexpr int kMpk3Rows = 32;               // tile rows (y)
+constexpr int kMpk3Warps = kMpk3Rows / 2;   // two tile rows per warp
+constexpr int kMpk3Pad = kMpk3Rows + 2;     // shared plane rows (zero rows −1 and 32)
 
 template <int S, bool JAC>
 __global__ void __launch_bounds__(kMpk3Warps * 32, 1)
@@ -494,91 +498,133 @@ __global__ void __launch_bounds__(kMpk3Warps * 32, 1)
     KB_PDL_WAIT();
     constexpr int H = (S + 1) & ~1;
     constexpr int STEPX = 64 - 2 * H;
-    constexpr int STEPY = kMpk3Warps - 2 * S;
-    constexpr int ROW = 32;  // double2 per tile row
-    constexpr int PLANE = kMpk3Warps * ROW;  // double2 per tile plane
-    extern __shared__ double2 sm3[];  // [2 slots][S levels][32 rows][32 lanes]
+    constexpr int STEPY = kMpk3Rows - 2 * S;
+    constexpr int PLANE = kMpk3Pad * 32;  // double2 per shared plane
+    extern __shared__ double2 sm3[];      // [2 slots][S levels][kMpk3Pad rows][32 lanes]
     const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int r0 = 2 * w;  // tile rows r0, r0 + 1
     const int nx = static_cast<int>(g.nx), ny = static_cast<int>(g.ny), nz = static_cast<int>(g.nz);
     const int nzl = static_cast<int>(g.nzl), z0 = static_cast<int>(g.z0);
     const i64 nx64 = nx, plane = static_cast<i64>(nx) * ny;
+    const double c = g.c_off;
     for (int task = blockIdx.x; task < ntasks; task += gridDim.x) {
         const int wx = task % nwx, wy = (task / nwx) % nwy, wz = task / (nwx * nwy);
-        const int ix = wx * STEPX - H + 2 * lane, iy = wy * STEPY - S + w;
-        const bool in_plane = ix >= 0 && ix < nx && iy >= 0 && iy < ny;  // nx even: both columns or neither
-        const bool store_cell = in_plane && lane >= H / 2 && lane < 32 - H / 2 && w >= S && w < kMpk3Warps - S;
+        const int tx0 = wx * STEPX - H, ty0 = wy * STEPY - S;  // tile origin
+        const int ix = tx0 + 2 * lane, iy = ty0 + r0;
+        const bool inx = ix >= 0 && ix < nx;  // nx even: both columns or neither
+        const bool in0 = inx && iy >= 0 && iy < ny, in1 = inx && iy + 1 >= 0 && iy + 1 < ny;
+        const bool tile_inside = tx0 >= 0 && tx0 + 64 <= nx && ty0 >= 0 && ty0 + kMpk3Rows <= ny;
+        const bool st_lane = lane >= H / 2 && lane < 32 - H / 2;
+        const bool st0 = st_lane && in0 && r0 >= S && r0 < kMpk3Rows - S;
+        const bool st1 = st_lane && in1 && r0 + 1 >= S && r0 + 1 < kMpk3Rows - S;
         const int zb0 = wz * band, zb1 = min(zb0 + band, nzl);
-        const int zs = max(zb0 - S, -z0);             // first input plane (local index)
-        const int zmax = min(nzl + S, nz - z0);       // first plane with no data (zeros above)
+        const int zs = max(zb0 - S, -z0);        // first input plane (local index)
+        const int zmax = min(nzl + S, nz - z0);  // first plane with no data (zeros above)
         const int steps = zb1 - zs + S;
         const i64 cell = static_cast<i64>(iy) * nx64 + ix;
-        auto load = [&](int l) -> double2 {
-            double2 v = make_double2(0.0, 0.0);
-            if (in_plane && l < zmax) {
-                const double* p = l < 0       ? halo_lo + static_cast<i64>(l + S) * plane
-                                  : l < nzl ? x + static_cast<i64>(l) * plane
-                                            : halo_hi + static_cast<i64>(l - nzl) * plane;
-                v = __ldg(reinterpret_cast<const double2*>(p + cell));
-            }
-            return v;
+        // input plane l, rows r0 and r0 + 1 (+0.0 outside the grid)
+        auto load2 = [&](int l, double2& v0, double2& v1) {
+            v0 = v1 = make_double2(0.0, 0.0);
+            if (l >= zmax) return;
+            const double* p = (l >= 0 && l < nzl) ? x + static_cast<i64>(l) * plane
+                              : l < 0           ? halo_lo + static_cast<i64>(l + S) * plane
+                                                : halo_hi + static_cast<i64>(l - nzl) * plane;
+            p += cell;
+            if (in0) v0 = __ldg(reinterpret_cast<const double2*>(p));
+            if (in1) v1 = __ldg(reinterpret_cast<const double2*>(p + nx64));
         };
-        // h2[j]: level j's column at the plane of step t − 2 (the step t − 1
-        // plane is read back from the shared slot, with the y-neighbours).
-        double2 h2[S];
+        // a0/a1[j]: level j's two rows at the plane of step t − 1 (registers);
+        // the plane of step t − 2 is this thread's own cell of shared slot t & 1,
+        // read just before this step's value of the level replaces it
+        double2 a0[S], a1[S];
 #pragma unroll
-        for (int j = 0; j < S; ++j) h2[j] = make_double2(0.0, 0.0);
-        double2 pf0 = load(zs), pf1 = load(zs + 1);
+        for (int j = 0; j < S; ++j) a0[j] = a1[j] = make_double2(0.0, 0.0);
+        double2 pf[2][2];  // input planes of steps t, t + 1 (ring by step parity)
+        load2(zs, pf[0][0], pf[0][1]);
+        load2(zs + 1, pf[1][0], pf[1][1]);
         __syncthreads();  // the previous task's last reads of the shared planes are done
-        // the "step −1" planes (slot 1): +0.0, what lies below the grid's first plane
-#pragma unroll
-        for (int j = 0; j < S; ++j) sm3[(1 * S + j) * PLANE + w * ROW + lane] = make_double2(0.0, 0.0);
+        // zero both slots (the "step −1" and "step −2" planes and the padding rows)
+        for (int i = threadIdx.x; i < 2 * S * PLANE; i += blockDim.x) sm3[i] = make_double2(0.0, 0.0);
         __syncthreads();
-        for (int t = 0; t < steps; ++t) {
-            const int cur = t & 1, prv = cur ^ 1;
-            double2 up = pf0;  // level 0 (the input) at plane zs + t
-            pf0 = pf1;
-            pf1 = load(zs + t + 2);
-            sm3[(cur * S + 0) * PLANE + w * ROW + lane] = up;
+        double2* const mine = sm3 + (r0 + 1) * 32 + lane;  // padded row r0 + 1 ↔ tile row r0
+        double* const orow = out + cell;
+        // one step: P = t mod 2 selects the prefetch slot (unrolled by two so
+        // the ring never moves; the next load goes out after the slot's last use)
+        auto step = [&](auto parity, int t) {
+            constexpr int P = decltype(parity)::value;
+            const int cur = P, prv = P ^ 1;
+            const int lt = zs + t;  // input plane this step
+            // every level's plane this step inside the grid and the band: no masks
+            const bool fast = tile_inside && lt - S >= max(zb0, -z0) && lt - 1 < min(zb1, nz - z0);
+            double2 u0 = pf[P][0], u1 = pf[P][1];  // level 0 (the input) at plane lt
 #pragma unroll
             for (int k = 1; k <= S; ++k) {
-                const int l = zs + t - k;  // level k's plane this step
-                const int gz = z0 + l;
-                const double2* pl = sm3 + (prv * S + (k - 1)) * PLANE + w * ROW + lane;
-                const double2 cu = pl[0];
-                const double2 ym = w > 0 ? pl[-ROW] : make_double2(0.0, 0.0);
-                const double2 yp = w + 1 < kMpk3Warps ? pl[ROW] : make_double2(0.0, 0.0);
-                const double2 dn = h2[k - 1];
-                h2[k - 1] = cu;
-                const double left = __shfl_up_sync(0xffffffffu, cu.y, 1);
-                const double right = __shfl_down_sync(0xffffffffu, cu.x, 1);
-                double s0 = off_term<JAC>(0.0, g.c_off, dn.x);
-                s0 = off_term<JAC>(s0, g.c_off, ym.x);
-                s0 = off_term<JAC>(s0, g.c_off, left);
-                s0 = diag_term<JAC>(s0, 6.0, cu.x);
-                s0 = off_term<JAC>(s0, g.c_off, cu.y);
-                s0 = off_term<JAC>(s0, g.c_off, yp.x);
-                s0 = off_term<JAC>(s0, g.c_off, up.x);
-                double s1 = off_term<JAC>(0.0, g.c_off, dn.y);
-                s1 = off_term<JAC>(s1, g.c_off, ym.y);
-                s1 = off_term<JAC>(s1, g.c_off, cu.x);
-                s1 = diag_term<JAC>(s1, 6.0, cu.y);
-                s1 = off_term<JAC>(s1, g.c_off, right);
-                s1 = off_term<JAC>(s1, g.c_off, yp.y);
-                s1 = off_term<JAC>(s1, g.c_off, up.y);
-                // outside the grid: exactly +0.0 (an absent neighbour of a valid cell)
-                const bool live = in_plane && gz >= 0 && gz < nz;
-                const double2 v = live ? make_double2(s0, s1) : make_double2(0.0, 0.0);
-                if (store_cell && l >= zb0 && l < zb1)
-                    *reinterpret_cast<double2*>(out + static_cast<i64>(k - 1) * ldo + static_cast<i64>(l) * plane +
-                                                cell) = v;
-                if (k < S) sm3[(cur * S + k) * PLANE + w * ROW + lane] = v;
-                up = v;  // level k at plane l is level k + 1's upper neighbour
+                const int l = lt - k;  // level k's plane this step
+                double2* const qc = mine + (cur * S + (k - 1)) * PLANE;   // level k − 1, slot t (holds t − 2)
+                const double2* const qp = mine + (prv * S + (k - 1)) * PLANE;  // level k − 1, slot t − 1
+                const double2 dn0 = qc[0], dn1 = qc[32];
+                qc[0] = u0;  // publish level k − 1's plane of this step
+                qc[32] = u1;
+                const double2 cu0 = a0[k - 1], cu1 = a1[k - 1];
+                a0[k - 1] = u0;
+                a1[k - 1] = u1;
+                const double2 ym0 = qp[-32], yp1 = qp[64];
+                const double l0 = __shfl_up_sync(0xffffffffu, cu0.y, 1), r0v = __shfl_down_sync(0xffffffffu, cu0.x, 1);
+                const double l1 = __shfl_up_sync(0xffffffffu, cu1.y, 1), r1v = __shfl_down_sync(0xffffffffu, cu1.x, 1);
+                // row r0: y−1 from the shared plane, y+1 = this thread's row r0 + 1
+                double s0 = off_term<JAC>(0.0, c, dn0.x);
+                s0 = off_term<JAC>(s0, c, ym0.x);
+                s0 = off_term<JAC>(s0, c, l0);
+                s0 = diag_term<JAC>(s0, 6.0, cu0.x);
+                s0 = off_term<JAC>(s0, c, cu0.y);
+                s0 = off_term<JAC>(s0, c, cu1.x);
+                s0 = off_term<JAC>(s0, c, u0.x);
+                double s1 = off_term<JAC>(0.0, c, dn0.y);
+                s1 = off_term<JAC>(s1, c, ym0.y);
+                s1 = off_term<JAC>(s1, c, cu0.x);
+                s1 = diag_term<JAC>(s1, 6.0, cu0.y);
+                s1 = off_term<JAC>(s1, c, r0v);
+                s1 = off_term<JAC>(s1, c, cu1.y);
+                s1 = off_term<JAC>(s1, c, u0.y);
+                // row r0 + 1: y−1 = this thread's row r0, y+1 from the shared plane
+                double s2 = off_term<JAC>(0.0, c, dn1.x);
+                s2 = off_term<JAC>(s2, c, cu0.x);
+                s2 = off_term<JAC>(s2, c, l1);
+                s2 = diag_term<JAC>(s2, 6.0, cu1.x);
+                s2 = off_term<JAC>(s2, c, cu1.y);
+                s2 = off_term<JAC>(s2, c, yp1.x);
+                s2 = off_term<JAC>(s2, c, u1.x);
+                double s3 = off_term<JAC>(0.0, c, dn1.y);
+                s3 = off_term<JAC>(s3, c, cu0.y);
+                s3 = off_term<JAC>(s3, c, cu1.x);
+                s3 = diag_term<JAC>(s3, 6.0, cu1.y);
+                s3 = off_term<JAC>(s3, c, r1v);
+                s3 = off_term<JAC>(s3, c, yp1.y);
+                s3 = off_term<JAC>(s3, c, u1.y);
+                double2 v0 = make_double2(s0, s1), v1 = make_double2(s2, s3);
+                if (!fast) {
+                    // outside the grid: exactly +0.0 (an absent neighbour of a valid cell)
+                    const int gz = z0 + l;
+                    const bool zin = gz >= 0 && gz < nz;
+                    if (!(in0 && zin)) v0 = make_double2(0.0, 0.0);
+                    if (!(in1 && zin)) v1 = make_double2(0.0, 0.0);
+                }
+                const bool lin = fast || (l >= zb0 && l < zb1);
+                double* const o = orow + static_cast<i64>(k - 1) * ldo + static_cast<i64>(l) * plane;
+                if (lin && st0) *reinterpret_cast<double2*>(o) = v0;
+                if (lin && st1) *reinterpret_cast<double2*>(o + nx64) = v1;
+                u0 = v0;  // level k at plane l: level k + 1's upper neighbour
+                u1 = v1;
             }
+            load2(lt + 2, pf[P][0], pf[P][1]);
             __syncthreads();
+        };
+        for (int t = 0; t < steps; t += 2) {
+            step(std::integral_constant<int, 0>{}, t);
+            if (t + 1 < steps) step(std::integral_constant<int, 1>{}, t + 1);
         }
     }
 }
-
 
 // CSR SpMV, one warp per 32 consecutive rows, in two phases per chunk of
 // the warp's contiguous nnz range (kCsrChunk entries):
@@ -849,12 +895,12 @@ void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const 
 
 bool mpk3d_supported(const StencilGeom& g, int s, const double* x, const double* out, i64 ldo, bool force) {
     auto a16 = [](const void* p) { return (reinterpret_cast<uintptr_t>(p) & 15) == 0; };
-    if (!(g.dims == 3 && (g.nx & 1) == 0 && s >= 1 && s <= 7 && (ldo & 1) == 0 && a16(x) && a16(out) &&
+    if (!(g.dims == 3 && (g.nx & 1) == 0 && s >= 1 && s <= 6 && (ldo & 1) == 0 && a16(x) && a16(out) &&
           g.nzl >= 1 && g.nx + 64 < (i64(1) << 31) && g.ny + 64 < (i64(1) << 31) && g.nz + 16 < (i64(1) << 31)))
         return false;
     // Worth it once the (tile, band) tasks fill the GPU with one CTA per SM.
     const int h = (s + 1) & ~1;
-    const i64 tiles = ceil_div(g.nx, 64 - 2 * h) * ceil_div(g.ny, kMpk3Warps - 2 * s);
+    const i64 tiles = ceil_div(g.nx, 64 - 2 * h) * ceil_div(g.ny, kMpk3Rows - 2 * s);
     const i64 tasks = tiles * std::max<i64>(1, g.nzl / (4 * s));
     return force || tasks >= static_cast<i64>(num_sms());
 }
@@ -863,7 +909,7 @@ void launch_mpk3d(cudaStream_t st, const StencilGeom& g, const double* x, const 
                   const double* halo_hi, double* out, i64 ldo, int s, int64_t& launches) {
     const bool jacobi = g.jacobi != 0;
     const int h = (s + 1) & ~1;
-    const i64 nwx = ceil_div(g.nx, 64 - 2 * h), nwy = ceil_div(g.ny, kMpk3Warps - 2 * s);
+    const i64 nwx = ceil_div(g.nx, 64 - 2 * h), nwy = ceil_div(g.ny, kMpk3Rows - 2 * s);
     const i64 sms = num_sms();
     // z-bands per tile: minimise rounds × (band + 2s) steps per CTA (one CTA per SM)
     i64 nzb = 1, best = -1;
@@ -879,7 +925,7 @@ void launch_mpk3d(cudaStream_t st, const StencilGeom& g, const double* x, const 
     nzb = ceil_div(g.nzl, band);
     const i64 ntasks = nwx * nwy * nzb;
     if (ntasks >= (i64(1) << 31)) fail(KRY_UNSUPPORTED, "mpk3d: too many tiles");
-    const size_t smem = static_cast<size_t>(2 * s) * kMpk3Warps * 32 * sizeof(double2);
+    const size_t smem = static_cast<size_t>(2 * s) * kMpk3Pad * 32 * sizeof(double2);
     const unsigned grid = static_cast<unsigned>(std::min<i64>(ntasks, sms));
     auto go = [&](auto kernel) {
         set_kernel_smem(reinterpret_cast<const void*>(kernel), smem);
@@ -898,7 +944,6 @@ void launch_mpk3d(cudaStream_t st, const StencilGeom& g, const double* x, const 
         KB_MPK3(4)
         KB_MPK3(5)
         KB_MPK3(6)
-        KB_MPK3(7)
         default: fail(KRY_INTERNAL, "mpk3d: unsupported s");
     }
 #undef KB_MPK3

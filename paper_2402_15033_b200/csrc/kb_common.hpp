@@ -47,6 +47,21 @@ inline void dim_check(bool ok, const char* what) {
             ::kb::fail(KRY_CUDA_ERROR, std::string("kernel launch: ") + cudaGetErrorString(kb_e_)); \
     } while (0)
 
+// CUDA-graph replay of a recorded launch sequence (kb_gmres.cpp): while the
+// host re-runs a sequence whose kernels a cached graph already holds, the
+// launch wrappers (launch_pdl) skip the launch; the host bookkeeping and the
+// launch counters still run.
+inline bool& launches_suppressed() {
+    static thread_local bool on = false;
+    return on;
+}
+// Bumped whenever a device buffer is (re)allocated: a recorded graph holds
+// raw pointers, so it is replayed only while the generation is unchanged.
+inline uint64_t& devbuf_generation() {
+    static uint64_t g = 0;
+    return g;
+}
+
 inline i64 ceil_div(i64 a, i64 b) { return (a + b - 1) / b; }
 inline i64 round_up(i64 a, i64 b) { return ceil_div(a, b) * b; }
 

@@ -10,6 +10,7 @@
 #include <vector>
 
 #include "kb_common.hpp"
+#include "nvtx3/nvToolsExt.h"
 
 namespace kb {
 
@@ -39,6 +40,7 @@ struct DevBuf {
         KB_CUDA(cudaMalloc(&q, b));
         p = static_cast<double*>(q);
         bytes = b;
+        ++devbuf_generation();
     }
     template <typename T> T* as() const { return reinterpret_cast<T*>(p); }
 };
@@ -114,5 +116,14 @@ struct Ctx {
 
 // Host thread-local: device of the current call.
 void bind_device(Ctx& c);
+
+// NVTX range for a profiler timeline (nsys / ncu --nvtx); a no-op unless a
+// tool is attached.  Scoped: pushed on construction, popped on destruction.
+struct NvtxRange {
+    explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+    ~NvtxRange() { nvtxRangePop(); }
+    NvtxRange(const NvtxRange&) = delete;
+    NvtxRange& operator=(const NvtxRange&) = delete;
+};
 
 }  // namespace kb

@@ -46,11 +46,13 @@ inline cudaLaunchConfig_t pdl_config(dim3 grid, dim3 block, size_t smem, cudaStr
 template <typename... KArgs, typename... Args>
 inline void launch_pdl(void (*kernel)(KArgs...), dim3 grid, dim3 block, size_t smem, cudaStream_t s,
                        Args&&... args) {
+    if (launches_suppressed()) return;
     cudaLaunchAttribute at[1];
     const cudaLaunchConfig_t cfg = pdl_config(grid, block, smem, s, at);
     KB_CUDA(cudaLaunchKernelEx(&cfg, kernel, std::forward<Args>(args)...));
 }
 inline void launch_pdl_c(const void* kernel, dim3 grid, dim3 block, size_t smem, cudaStream_t s, void** args) {
+    if (launches_suppressed()) return;
     cudaLaunchAttribute at[1];
     const cudaLaunchConfig_t cfg = pdl_config(grid, block, smem, s, at);
     KB_CUDA(cudaLaunchKernelExC(&cfg, kernel, args));

@@ -37,6 +37,47 @@ Workspace::~Workspace() {
     if (copy_stream) cudaStreamDestroy(copy_stream);
 }
 
+namespace {
+struct L2Window {
+    Ctx& ctx;
+    bool set = false;
+    L2Window(Ctx& c, const double* q, i64 ld) : ctx(c) {
+        const char* e = std::getenv("KRY_L2_PERSIST");
+        if (e && std::atoi(e) == 0) return;
+        int dev = 0, maxwin = 0, maxpersist = 0;
+        if (cudaGetDevice(&dev) != cudaSuccess) return;
+        cudaDeviceGetAttribute(&maxwin, cudaDevAttrMaxAccessPolicyWindowSize, dev);
+        cudaDeviceGetAttribute(&maxpersist, cudaDevAttrMaxPersistingL2CacheSize, dev);
+        const size_t col = static_cast<size_t>(ld) * 8;
+        const size_t cap = std::min<size_t>(static_cast<size_t>(maxpersist), static_cast<size_t>(maxwin));
+        if (cap == 0 || 2 * col > cap) return;  // fewer than two columns would fit: no gain
+        const size_t bytes = cap / col * col;
+        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.base_ptr = const_cast<double*>(q);
+        v.accessPolicyWindow.num_bytes = bytes;
+        v.accessPolicyWindow.hitRatio = 1.0f;
+        v.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+        v.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+        if (cudaStreamSetAttribute(ctx.stream, cudaStreamAttributeAccessPolicyWindow, &v) != cudaSuccess) {
+            cudaGetLastError();
+            return;
+        }
+        set = true;
+    }
+    ~L2Window() {
+        if (!set) return;
+        cudaStreamAttrValue v{};
+        v.accessPolicyWindow.num_bytes = 0;
+        cudaStreamSetAttribute(ctx.stream, cudaStreamAttributeAccessPolicyWindow, &v);
+        cudaCtxResetPersistingL2Cache();
+    }
+};
+}  // namespace
+
 Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, const kry_solver_config& cfg_in,
              bool standard_mode, double* d_x_out, Workspace* ws, double* h_x_out) {
     kry_solver_config cfg = cfg_in;
@@ -132,6 +173,12 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
 
     if (!W.store) W.store = std::make_unique<Store>(ctx, n, m, s, shat);
     Store& store = *W.store;
+    // Small grids: the basis prefix is re-read by every block's Gram and
+    // update (twice per block), and at 512² the whole store (128 MB) is about
+    // the size of L2 — an LRU sweep over it misses almost every line.  Pin
+    // the leading columns in L2 with a persisting access-policy window on the
+    // solver stream (KRY_L2_PERSIST=0 disables); released on every exit.
+    L2Window l2win(ctx, store.col(0), store.ld());
     store.ortho_bytes = 0.0;
     const int scheme = cfg.scheme_kind;
 
@@ -181,6 +228,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
         const std::vector<double>& ycoef = cache.ycoef;
         res.implicit_crossed = lsq.implicit_residual <= cfg.rel_tol * r0;
         if (!res.implicit_crossed && !force) return res;
+        NvtxRange nv("kry.solution_update");
 
         cudaEvent_t t0 = ctx.begin_phase();
         // x_new = x + Q·y in row chunks; with a host output each chunk is
@@ -225,6 +273,75 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
         return res;
     };
 
+    // Speculative queues replayed as CUDA graphs (one rank, no phase timing:
+    // the recorded launches hold no events).  Opt-in (KRY_GRAPHS=1): at 512²
+    // the cycle is bound by the kernels' own latencies, not by the host's
+    // launch rate — 0.0838 vs 0.0835 s two-stage, 0.1275 vs 0.1277 s PIP2
+    // (DESIGN.md §5), so the direct launches stay the default.
+    const bool use_graphs = [] {
+        const char* e = std::getenv("KRY_GRAPHS");
+        return e && std::atoi(e) == 1;
+    }() && ctx.nranks == 1 && !ctx.timing;
+    if (use_graphs) {
+        const char* fm = std::getenv("KRY_FUSED_MPK");
+        const std::string sig = std::to_string(reinterpret_cast<uintptr_t>(&op)) + "/" +
+                                std::to_string(op.geom.jacobi) + "/" + std::to_string(op.jacobi) + "/" +
+                                (fm ? fm : "-") + "/" + std::to_string(cfg.scheme_kind) + "/" +
+                                std::to_string(s) + "/" + std::to_string(shat);
+        if (sig != W.graphs.sig) {
+            W.graphs.clear();
+            W.graphs.sig = sig;
+        }
+    }
+    // body() enqueues a launch sequence (and does its host bookkeeping).
+    // First time for `key`: record it (stream capture) and replay the graph;
+    // later: run body() with the launches suppressed and replay the graph —
+    // valid while no device buffer was reallocated since the recording.
+    auto recorded = [&](uint64_t key, auto&& body) {
+        if (!use_graphs) {
+            body();
+            return;
+        }
+        for (auto& e : W.graphs.entries) {
+            if (e.key != key || e.gen != devbuf_generation()) continue;
+            launches_suppressed() = true;
+            try {
+                body();
+            } catch (...) {
+                launches_suppressed() = false;
+                throw;
+            }
+            launches_suppressed() = false;
+            if (e.gen != devbuf_generation()) fail(KRY_INTERNAL, "graph replay: a device buffer moved");
+            KB_CUDA(cudaGraphLaunch(e.exec, ctx.stream));
+            return;
+        }
+        KB_CUDA(cudaStreamBeginCapture(ctx.stream, cudaStreamCaptureModeRelaxed));
+        try {
+            body();
+        } catch (...) {
+            cudaGraph_t g = nullptr;
+            cudaStreamEndCapture(ctx.stream, &g);
+            if (g) cudaGraphDestroy(g);
+            throw;
+        }
+        cudaGraph_t g = nullptr;
+        KB_CUDA(cudaStreamEndCapture(ctx.stream, &g));
+        cudaGraphExec_t exec = nullptr;
+        const cudaError_t ie = cudaGraphInstantiate(&exec, g, 0);
+        cudaGraphDestroy(g);
+        KB_CUDA(ie);
+        for (auto it = W.graphs.entries.begin(); it != W.graphs.entries.end();)
+            if (it->key == key) {
+                cudaGraphExecDestroy(it->exec);
+                it = W.graphs.entries.erase(it);
+            } else {
+                ++it;
+            }
+        W.graphs.entries.push_back({key, devbuf_generation(), exec});
+        KB_CUDA(cudaGraphLaunch(exec, ctx.stream));
+    };
+
     // read per solve (tests switch them between solves)
     const bool speculate_default = [] {  // KRY_SPECULATE=0: every block waits for its factorisation
         const char* e = std::getenv("KRY_SPECULATE");
@@ -248,6 +365,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
             rep.status = KRY_STATUS_MAX_ITERS;
             break;
         }
+        NvtxRange nv_cycle("kry.cycle");
         store.reset();
         {
             cudaEvent_t t0 = ctx.begin_phase();
@@ -258,6 +376,11 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
 
         bool updated_this_cycle = false;
         bool speculate = speculate_default && two_stage && store.can_speculate(s + 1);
+        // one-stage BCGS-PIP2: the rest of the cycle is queued without host
+        // waits (both passes factorised on the device) and replayed block by
+        // block, so the per-block convergence check keeps its place
+        bool spec_pip2 = speculate_default && !two_stage && !standard_mode && scheme == KRY_ORTHO_BCGS_PIP2 &&
+                         store.can_speculate_pip2(s + 1);
         bool skip_mpk = false;  // a speculative block being redone: its raw columns are in place
         for (i64 j = 0; j < blocks && !done; ++j) {
             Outcome oc;
@@ -270,32 +393,40 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
                 // 2-D stencil on one rank: block j's update, block j+1's MPK
                 // and Gram in one pass (K6, k_fused.cu); the MPK is then part
                 // of the BlkOrtho phase.
+                NvtxRange nv("kry.speculative_panel");
                 const i64 j0 = j;
                 i64 jj = j;
                 const bool fuse = store.can_fuse(op, s);
-                for (;;) {
-                    if (fuse) {
-                        cudaEvent_t t1 = ctx.begin_phase();
-                        if (jj == j0)
-                            store.spec_fused_first(op, s, jj != 0);
-                        else
-                            store.spec_fused_next(op, s);
-                        ctx.end_phase(PH_ORTHO, t1);
-                        rep.mpk_bytes += 8.0 * op.nloc * (s + 1.0);
-                    } else {
-                        const i64 c0 = (jj == 0) ? 0 : store.spec_filled() - 1;
-                        cudaEvent_t t0 = ctx.begin_phase();
-                        rep.mpk_bytes += store.mpk(op, c0, s) ? 8.0 * op.nloc * (s + 1.0) : s * op.bytes_per_apply();
-                        ctx.end_phase(PH_MPK, t0);
-                        cudaEvent_t t1 = ctx.begin_phase();
-                        store.preprocess_speculative(s + 1, jj != 0);
-                        ctx.end_phase(PH_ORTHO, t1);
+                auto queue_panel = [&] {
+                    jj = j0;
+                    for (;;) {
+                        if (fuse) {
+                            cudaEvent_t t1 = ctx.begin_phase();
+                            if (jj == j0)
+                                store.spec_fused_first(op, s, jj != 0);
+                            else
+                                store.spec_fused_next(op, s);
+                            ctx.end_phase(PH_ORTHO, t1);
+                            rep.mpk_bytes += 8.0 * op.nloc * (s + 1.0);
+                        } else {
+                            const i64 c0 = (jj == 0) ? 0 : store.spec_filled() - 1;
+                            cudaEvent_t t0 = ctx.begin_phase();
+                            rep.mpk_bytes += store.mpk(op, c0, s) ? 8.0 * op.nloc * (s + 1.0) : s * op.bytes_per_apply();
+                            ctx.end_phase(PH_MPK, t0);
+                            cudaEvent_t t1 = ctx.begin_phase();
+                            store.preprocess_speculative(s + 1, jj != 0);
+                            ctx.end_phase(PH_ORTHO, t1);
+                        }
+                        ++jj;
+                        if (store.spec_panel_full() || jj == blocks) break;
                     }
-                    ++jj;
-                    if (store.spec_panel_full() || jj == blocks) break;
-                }
+                    store.spec_flush();
+                };
+                if (fuse)
+                    queue_panel();
+                else
+                    recorded((uint64_t(1) << 60) | (uint64_t(j0) << 30) | uint64_t(store.filled()), queue_panel);
                 cudaEvent_t t1 = ctx.begin_phase();
-                store.spec_flush();
                 const i64 f = store.resolve_speculative(rep.sync);
                 ctx.end_phase(PH_ORTHO, t1);
                 rep.iterations += s * (f < 0 ? jj - j0 : f);
@@ -307,6 +438,35 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
                 }
                 j = jj - 1;  // the panel's last block: finalize / check below
                 oc.committed = s + 1;
+            } else if (spec_pip2) {
+                if (!store.spec_has_next()) {
+                    NvtxRange nv("kry.speculative_pip2_cycle");
+                    recorded((uint64_t(2) << 60) | (uint64_t(j) << 30) | uint64_t(store.filled()), [&] {
+                        for (i64 jj = j; jj < blocks; ++jj) {
+                            const i64 c0 = (jj == 0) ? 0 : store.spec_filled() - 1;
+                            cudaEvent_t t0 = ctx.begin_phase();
+                            rep.mpk_bytes +=
+                                store.mpk(op, c0, s) ? 8.0 * op.nloc * (s + 1.0) : s * op.bytes_per_apply();
+                            ctx.end_phase(PH_MPK, t0);
+                            cudaEvent_t t1 = ctx.begin_phase();
+                            store.preprocess_speculative_pip2(s + 1, jj != 0);
+                            ctx.end_phase(PH_ORTHO, t1);
+                        }
+                    });
+                    cudaEvent_t t1 = ctx.begin_phase();
+                    store.spec_fetch();
+                    ctx.end_phase(PH_ORTHO, t1);
+                }
+                if (store.spec_commit_next(rep.sync) != 1) {
+                    // the factorisation failed (or the queue is off): redo this
+                    // block on the synchronous path, raw columns in place
+                    store.spec_drop();
+                    spec_pip2 = false;
+                    skip_mpk = true;
+                    --j;
+                    continue;
+                }
+                oc.committed = s + 1;
             } else if (standard_mode) {
                 const i64 f = store.filled();
                 cudaEvent_t t0 = ctx.begin_phase();
@@ -317,6 +477,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
                 oc = store.append_block(store.col(f), store.ld(), 1, false, scheme, 0, rep.sync);
                 ctx.end_phase(PH_ORTHO, t1);
             } else {
+                NvtxRange nv("kry.block");
                 const i64 c0 = (j == 0) ? 0 : store.filled() - 1;
                 if (!skip_mpk) {
                     cudaEvent_t t0 = ctx.begin_phase();
@@ -353,6 +514,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
             if (two_stage) {
                 const bool last_block = (j + 1 == blocks);
                 if (store.big_panel_full() || last_block) {
+                    NvtxRange nv("kry.finalize_big_panel");
                     cudaEvent_t t1 = ctx.begin_phase();
                     // The cycle's last panel is only read by the solution update:
                     // defer its (15.6 GB at 4000²) rewrite into the y coefficients.
@@ -385,6 +547,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
             }
         }
 
+        store.spec_drop();  // speculative PIP2 blocks past an early end of the cycle
         if (!updated_this_cycle) check_and_update(gamma, true);
         const double rnorm = r_norm;
         rep.cycle_residuals.push_back(rnorm / r0);

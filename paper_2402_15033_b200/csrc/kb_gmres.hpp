@@ -6,6 +6,7 @@
 #pragma once
 
 #include <memory>
+#include <string>
 #include <vector>
 
 #include "kb_operator.hpp"
@@ -32,8 +33,27 @@ struct Report {
 // Device workspace of one solve (basis store + four vectors), kept by the
 // C-ABI context so that repeated solves of the same shape reuse HBM instead
 // of re-allocating (and re-zeroing) an n×(m+1) basis per call.
+// Recorded launch sequences of the speculative queues (one per cycle
+// position), replayed as CUDA graphs: a 512² cycle is ~70 (two-stage) to
+// ~110 (PIP2) launches whose host-side cost would otherwise bound it.
+struct GraphCache {
+    struct Entry {
+        uint64_t key;
+        uint64_t gen;
+        cudaGraphExec_t exec;
+    };
+    std::vector<Entry> entries;
+    std::string sig;  // operator / scheme / switches the recordings belong to
+    void clear() {
+        for (auto& e : entries) cudaGraphExecDestroy(e.exec);
+        entries.clear();
+    }
+    ~GraphCache() { clear(); }
+};
+
 struct Workspace {
     i64 n = -1, m = -1, s = -1, shat = -1;
+    GraphCache graphs;
     std::unique_ptr<Store> store;
     DevBuf x, xn, r, rn;
     DevBuf bj;  // D⁻¹b of a Jacobi-preconditioned operator

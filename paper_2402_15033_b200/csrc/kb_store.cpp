@@ -56,7 +56,7 @@ bool Store::deferred_coefficients(const std::vector<double>& y, std::vector<doub
 void Store::reset() {
     pending_ = false;
     fpend_.live = false;
-    spec_.clear();
+    spec_drop();
     std::fill(pready_.begin(), pready_.end(), 0);
     filled_ = 0;
     finalized_ = 0;
@@ -98,13 +98,13 @@ bool Store::spec_panel_full() const {
     return f > b && f - b >= big_panel_size_ + 1;
 }
 
-Store::SpecPlan Store::spec_plan(i64 w, bool overlap) {
+Store::SpecPlan Store::spec_plan(i64 w, bool overlap, bool pieces) {
     const bool first = spec_.empty();
     const i64 filled = first ? filled_ : spec_filled_;
     if (overlap && filled == 0) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: basis store capacity exceeded");
     const i64 c0 = overlap ? filled - 1 : filled;
     if (c0 + w > max_cols_) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: basis store capacity exceeded");
-    const i64 maxb = max_cols_;  // queue capacity (blocks per cycle ≤ m)
+    const i64 maxb = 2 * max_cols_;  // queue capacity in result slots (blocks per cycle ≤ m, 2 slots for PIP2)
     if (first) {
         spec_bps_ = big_panel_start_;
         spec_xd_ = big_panel_start_;
@@ -119,7 +119,7 @@ Store::SpecPlan Store::spec_plan(i64 w, bool overlap) {
     // previous block is a preprocessed block of the open panel unless this
     // is the panel's first block
     const bool prev_in_panel = !first || (!records_.empty() && states_.back() == KRY_PANEL_PREPROCESSED);
-    if (prev_in_panel) {
+    if (pieces && prev_in_panel) {
         const i64 xend = std::min(c0 / 8 * 8, spec_xd_ / 8 * 8 + 16);
         if (xend > spec_xd_) {
             p.xf = spec_xd_;
@@ -261,45 +261,133 @@ void Store::spec_flush() {
 
 i64 Store::resolve_speculative(Sync& sync) {
     if (spec_.empty()) return -1;
-    const size_t bytes = spec_.size() * kSlotDoubles * 8;
-    KB_CUDA(cudaMemcpyAsync(spec_host_.p, spec_slots_.p, bytes, cudaMemcpyDeviceToHost, ctx_.stream));
-    ctx_.sync();
+    spec_fetch();
     i64 failed = -1;
-    for (size_t i = 0; i < spec_.size(); ++i) {
-        const SpecBlock& b = spec_[i];
-        const double* slot = spec_host_.p + i * kSlotDoubles;
-        if (slot[kSlotStatus] != 0.0) {
+    for (size_t i = 0; i < spec_.size(); ++i)
+        if (spec_commit_next(sync) == 0) {
             failed = static_cast<i64>(i);
-            // fused path: the block's raw columns live outside the store;
-            // put them where the synchronous redo expects them
-            if (b.raw)
-                KB_CUDA(cudaMemcpy2DAsync(col(b.c0), ld_ * 8, b.raw, ld_ * 8, n_ * 8, b.w, cudaMemcpyDeviceToDevice,
-                                          ctx_.stream));
             break;
         }
-        OrthoRes res;
-        res.r_col = Mat(b.c0, b.w);
-        res.r_jj = Upper(b.w);
-        const double* rc = slot + kSlotRcol;
-        const double* rj = rc + b.c0 * b.w;
-        for (i64 j = 0; j < b.w; ++j) {
-            for (i64 l = 0; l < b.c0; ++l) res.r_col(l, j) = rc[l + j * b.c0];
-            for (i64 l = 0; l <= j; ++l) res.r_jj.at(l, j) = rj[l + j * b.w];
+    spec_drop();
+    return failed;
+}
+
+void Store::spec_fetch() {
+    if (spec_.empty()) return;
+    const size_t slots = spec_.size() * (spec_.front().pip2 ? 2 : 1);
+    KB_CUDA(cudaMemcpyAsync(spec_host_.p, spec_slots_.p, slots * kSlotDoubles * 8, cudaMemcpyDeviceToHost,
+                            ctx_.stream));
+    ctx_.sync();
+    spec_fetched_ = true;
+    spec_next_ = 0;
+}
+
+void Store::spec_drop() {
+    spec_.clear();
+    spec_fetched_ = false;
+    spec_next_ = 0;
+}
+
+namespace {
+// R_col and R_jj of one result slot (k_pip.cu layout)
+void slot_factors(const double* slot, i64 c0, i64 w, Mat& r_col, Upper& r_jj) {
+    r_col = Mat(c0, w);
+    r_jj = Upper(w);
+    const double* rc = slot + kSlotRcol;
+    const double* rj = rc + c0 * w;
+    for (i64 j = 0; j < w; ++j) {
+        for (i64 l = 0; l < c0; ++l) r_col(l, j) = rc[l + j * c0];
+        for (i64 l = 0; l <= j; ++l) r_jj.at(l, j) = rj[l + j * w];
+    }
+}
+}  // namespace
+
+int Store::spec_commit_next(Sync& sync) {
+    if (!spec_fetched_ || spec_next_ >= spec_.size()) return -1;
+    const size_t i = spec_next_;
+    const SpecBlock& b = spec_[i];
+    const double* slot = spec_host_.p + (b.pip2 ? 2 * i : i) * kSlotDoubles;
+    const bool failed = slot[kSlotStatus] != 0.0 || (b.pip2 && slot[kSlotDoubles + kSlotStatus] != 0.0);
+    if (failed) {
+        // fused path: the block's raw columns live outside the store;
+        // put them where the synchronous redo expects them
+        if (b.raw)
+            KB_CUDA(cudaMemcpy2DAsync(col(b.c0), ld_ * 8, b.raw, ld_ * 8, n_ * 8, b.w, cudaMemcpyDeviceToDevice,
+                                      ctx_.stream));
+        spec_next_ = spec_.size();
+        return 0;
+    }
+    ++spec_next_;
+    const i64 before = sync.reduces;
+    OrthoRes res;
+    if (b.pip2) {
+        // run_scheme BcgsPip2 (basis_store.hpp:220-239): R_col = R₁ + T_col·R_jj₁,
+        // R_jj = T_jj·R_jj₁ — the synchronous path's arithmetic (run_scheme).
+        OrthoRes first, second;
+        slot_factors(slot, b.c0, b.w, first.r_col, first.r_jj);
+        slot_factors(slot + kSlotDoubles, b.c0, b.w, second.r_col, second.r_jj);
+        res.r_col = std::move(first.r_col);
+        if (res.r_col.rows > 0) {
+            Mat rjj(b.w, b.w);
+            for (i64 j = 0; j < b.w; ++j)
+                for (i64 l = 0; l <= j; ++l) rjj(l, j) = first.r_jj(l, j);
+            Mat corr = mat_mul_nn(second.r_col, rjj);
+            for (i64 j = 0; j < res.r_col.cols; ++j)
+                for (i64 l = 0; l < res.r_col.rows; ++l) res.r_col(l, j) += corr(l, j);
         }
+        res.r_jj = tri_mul(second.r_jj, first.r_jj);
+        sync.add(2);
+        ortho_bytes += 2.0 * 8.0 * n_ * (2.0 * b.c0 + 3.0 * b.w);
+        commit(b.c0, b.overlap, res, b.w, KRY_PANEL_FINAL);
+    } else {
+        slot_factors(slot, b.c0, b.w, res.r_col, res.r_jj);
         const double* pieces = slot + kSlotPieces;
         for (i64 k = 0; k < b.x_count; ++k) {
             for (i64 l = 0; l < b.c0; ++l) pgram_(l, b.x_first + k) = pieces[l + k * b.c0];
             pready_[static_cast<size_t>(b.x_first + k)] = 1;
         }
         // preprocess_block → append_block bookkeeping (one reduce per block)
-        const i64 before = sync.reduces;
         sync.add(1);
         ortho_bytes += 8.0 * n_ * (2.0 * b.c0 + 3.0 * b.w);
         commit(b.c0, b.overlap, res, b.w, KRY_PANEL_PREPROCESSED);
-        sync.per_block.push_back(sync.reduces - before);
     }
-    spec_.clear();
-    return failed;
+    sync.per_block.push_back(sync.reduces - before);
+    return 1;
+}
+
+bool Store::can_speculate_pip2(i64 w) const {
+    // the device factorisation handles c0 ≤ 64, w ≤ 8, and every block's
+    // prefix must fit one 64-slot Gram group (as can_speculate)
+    return w >= 1 && w <= 8 && round_up(max_cols_ - w, 8) + 8 <= 64;
+}
+
+void Store::preprocess_speculative_pip2(i64 w, bool overlap) {
+    const SpecPlan p = spec_plan(w, overlap, /*pieces=*/false);
+    const i64 c0 = p.c0, b = static_cast<i64>(spec_.size());
+    double* s0 = scratch(0, w);
+    for (int pass = 0; pass < 2; ++pass) {
+        // pass 1: V (store columns) → scratch; pass 2: scratch → store columns
+        const double* V = pass == 0 ? col(c0) : s0;
+        double* out = pass == 0 ? s0 : col(c0);
+        SpecPlan q = p;
+        q.idx = 2 * b + pass;
+        std::vector<int> tiles;
+        cudaEvent_t t0 = ctx_.begin_phase();
+        launch_gram_pass(ctx_.stream, n_, c0 > 0 ? col(0) : nullptr, ld_, c0, V, ld_, w, true, ctx_.gram_partials.p,
+                         ctx_.gram_packed.p, tiles, ctx_.launches, -1, 0);
+        ctx_.end_phase(PH_GRAM, t0);
+        ctx_.gram_bytes += 8.0 * n_ * (c0 + w);
+        ctx_.gram_launches += 1;
+        const PipBlockArgs a = spec_factor(q, w);
+        cudaEvent_t t1 = ctx_.begin_phase();
+        launch_update(ctx_.stream, n_, c0 > 0 ? col(0) : nullptr, ld_, c0, V, ld_, w, a.coef, true, out, ld_,
+                      ctx_.launches, a.skip);
+        ctx_.end_phase(PH_UPDATE, t1);
+        ctx_.update_bytes += 8.0 * n_ * (c0 + 2.0 * w);
+        ctx_.update_launches += 1;
+    }
+    spec_push(p, w, overlap, nullptr);
+    spec_.back().pip2 = true;
 }
 
 bool Store::mpk(Operator& op, i64 c0, i64 s) {

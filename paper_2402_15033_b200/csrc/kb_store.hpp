@@ -90,6 +90,24 @@ public:
     void spec_fused_next(Operator& op, i64 s);
     void spec_flush();
     i64 resolve_speculative(Sync& sync);
+    // ---- speculative one-stage BCGS-PIP2 (run_scheme BcgsPip2,
+    // basis_store.hpp:220-239) -------------------------------------------
+    // preprocess_speculative_pip2() queues both passes of a block (Gram →
+    // [allreduce] → device factorisation → gated update, twice: V → scratch
+    // → store columns) without waiting.  The one-stage solver checks
+    // convergence after every block, so the queue is replayed one block at
+    // a time: spec_fetch() copies the result slots back (one sync),
+    // spec_commit_next() replays the next block's bookkeeping exactly as
+    // append_block() would (R = composed passes, 2 reduces) and returns 1,
+    // or 0 when that block's factorisation failed (its raw columns are
+    // intact for the synchronous redo), or −1 when the queue is exhausted;
+    // spec_drop() discards what is left (the cycle ended early).
+    bool can_speculate_pip2(i64 w) const;
+    void preprocess_speculative_pip2(i64 w, bool overlap);
+    void spec_fetch();
+    int spec_commit_next(Sync& sync);
+    bool spec_has_next() const { return spec_fetched_ && spec_next_ < spec_.size(); }
+    void spec_drop();
     i64 spec_filled() const { return spec_.empty() ? filled_ : spec_filled_; }
     bool spec_panel_full() const;
     // MPK into the store: column c0 holds the start; columns c0+1..c0+s.
@@ -127,11 +145,12 @@ private:
         bool overlap;
         i64 x_first, x_count;
         const double* raw;  // raw block outside the store (fused path) or nullptr
+        bool pip2 = false;  // one-stage BCGS-PIP2: result slots 2i (pass 1) and 2i + 1 (pass 2)
     };
     struct SpecPlan {
         i64 c0, idx, xf, xc;
     };
-    SpecPlan spec_plan(i64 w, bool overlap);
+    SpecPlan spec_plan(i64 w, bool overlap, bool pieces = true);
     PipBlockArgs spec_factor(const SpecPlan& p, i64 w);
     void spec_push(const SpecPlan& p, i64 w, bool overlap, const double* raw);
     struct FusedPending {
@@ -144,6 +163,8 @@ private:
     FusedPending fpend_;
     DevBuf fraw_[2];  // raw blocks of the fused path (double-buffered)
     std::vector<SpecBlock> spec_;
+    size_t spec_next_ = 0;      // next queued block to replay (after spec_fetch)
+    bool spec_fetched_ = false;
     i64 spec_filled_ = 0, spec_bps_ = 0, spec_xd_ = 0;
     DevBuf spec_slots_, spec_coef_, spec_skip_;
     HostBuf spec_host_;

@@ -68,8 +68,8 @@ def test_standard_gmres_identity(kb, ctx, ref):
         want.status, want.iterations, want.restarts, want.reduces, want.breakdown)
 
 
-@pytest.mark.parametrize("k", [9, 13, 14])
-def test_mid_panel_breakdown_speculative_matches_synchronous(kb, ctx, ref, monkeypatch, k):
+@pytest.mark.parametrize("k,kind,shat", [(9, 3, 60), (13, 3, 60), (14, 3, 60), (9, 2, 0), (13, 2, 0), (17, 2, 0)])
+def test_mid_panel_breakdown_speculative_matches_synchronous(kb, ctx, ref, monkeypatch, k, kind, shat):
     """A Krylov space of dimension k (k distinct eigenvalues) ends inside the
     first big panel: the block that hits it fails its Cholesky after earlier
     blocks of the same panel were committed.  The speculative first stage
@@ -81,7 +81,7 @@ def test_mid_panel_breakdown_speculative_matches_synchronous(kb, ctx, ref, monke
     reps = []
     for spec in ("1", "0"):
         monkeypatch.setenv("KRY_SPECULATE", spec)
-        got, want = run_both(kb, ref, rp, ci, vv, b, 3, 60)
+        got, want = run_both(kb, ref, rp, ci, vv, b, kind, shat)
         reps.append(got)
     spec_rep, sync_rep = reps
     assert spec_rep.breakdown and sync_rep.breakdown
@@ -94,3 +94,22 @@ def test_mid_panel_breakdown_speculative_matches_synchronous(kb, ctx, ref, monke
     # fails first is a rounding-floor decision (randomised
     # sweep), so the counts are not compared here.
     assert want.breakdown
+
+
+@pytest.mark.parametrize("grid,kind", [(64, 2), (100, 2), (16, 2)])
+def test_speculative_pip2_matches_synchronous(kb, ctx, monkeypatch, grid, kind):
+    """One-stage BCGS-PIP2 queued without host waits (both passes factorised
+    on the device, replayed block by block with the per-block convergence
+    check) reproduces the synchronous path bit for bit."""
+    op = kb.Laplace2D(grid, grid)
+    b = op.spmv(np.ones(op.n))
+    cfg = kb.SolverConfig(scheme=kb.OrthoScheme(kb.OrthoKind(kind), 0))
+    reps = []
+    for spec in ("1", "0"):
+        monkeypatch.setenv("KRY_SPECULATE", spec)
+        reps.append(kb.sstep_gmres(op, b, None, cfg))
+    a, s = reps
+    assert (int(a.status), a.iterations, a.restarts, a.sync.reduces) == (int(s.status), s.iterations, s.restarts,
+                                                                        s.sync.reduces)
+    assert a.sync.per_block == s.sync.per_block and a.cycle_residuals == s.cycle_residuals
+    np.testing.assert_array_equal(a.solution, s.solution)

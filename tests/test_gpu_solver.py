@@ -273,3 +273,23 @@ def test_randomised_parity_sweep(kb, ctx, ref):
     p = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "4", "80"],
                        capture_output=True, text=True, timeout=600, cwd=root)
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-2000:]
+
+
+@pytest.mark.parametrize("key", ["two_2d100_s60", "two_2d100_s20", "pip2_2d100", "two_3d16_s60", "pip2_2d64_warm",
+                                 "rand20k_two_s60_jac"])
+def test_graph_replay_matches_direct_launches(kb, ctx, ref, monkeypatch, key):
+    """The speculative queues replayed as CUDA graphs (recorded once per
+    cycle position, KRY_GRAPHS default) give the same report and solution
+    bits as launching every kernel directly (KRY_GRAPHS=0)."""
+    if key not in GOLDEN:
+        pytest.skip(f"{key} golden not generated")
+    reps = []
+    for graphs in ("1", "0"):
+        monkeypatch.setenv("KRY_GRAPHS", graphs)
+        rep, g = run_golden(kb, ref, key)
+        assert_parity(rep, g)
+        reps.append(rep)
+    a, b = reps
+    assert a.cycle_residuals == b.cycle_residuals and a.sync.per_block == b.sync.per_block
+    np.testing.assert_array_equal(a.solution, b.solution)
+    assert a.telemetry["gpu_launches"] == b.telemetry["gpu_launches"]

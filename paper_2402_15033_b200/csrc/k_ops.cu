@@ -898,11 +898,14 @@ bool mpk3d_supported(const StencilGeom& g, int s, const double* x, const double*
     if (!(g.dims == 3 && (g.nx & 1) == 0 && s >= 1 && s <= 6 && (ldo & 1) == 0 && a16(x) && a16(out) &&
           g.nzl >= 1 && g.nx + 64 < (i64(1) << 31) && g.ny + 64 < (i64(1) << 31) && g.nz + 16 < (i64(1) << 31)))
         return false;
-    // Worth it once the (tile, band) tasks fill the GPU with one CTA per SM.
-    const int h = (s + 1) & ~1;
-    const i64 tiles = ceil_div(g.nx, 64 - 2 * h) * ceil_div(g.ny, kMpk3Rows - 2 * s);
-    const i64 tasks = tiles * std::max<i64>(1, g.nzl / (4 * s));
-    return force || tasks >= static_cast<i64>(num_sms());
+    // Opt-in (force: KRY_FUSED_MPK=2).  Bit-identical, but slower than s
+    // separate stencil3d_vec launches on B200: 4.12 vs 3.40 ms of MPK per
+    // 256³ cycle — each z-step costs ~550 warp instructions per level set
+    // (the y-neighbour exchange through shared memory, one barrier per step,
+    // 1.7× redundant tile-overlap work at s = 5), so the kernel is issue- and
+    // latency-bound at 2.1 IPC while the per-SpMV kernels stream at 5.2 TB/s
+    // (profiles/ncu_mpk3d_r02.txt).
+    return force;
 }
 
 void launch_mpk3d(cudaStream_t st, const StencilGeom& g, const double* x, const double* halo_lo,

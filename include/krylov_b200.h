@@ -270,6 +270,10 @@ int kry_store_panel_states(kry_store* st, int32_t* states);    /* n_panel_states
 int kry_store_block_record(kry_store* st, int64_t index, int64_t* c0, int64_t* width, int32_t* overlap,
                            double* carried, double* carried_diag);
 int kry_store_device_ptr(kry_store* st, double** d_q, int64_t* ld);
+/* Debug (KRY_GUARD=1 at store creation): KRY_INTERNAL if any kernel wrote the
+ * store's guard columns or padding rows [n, ld); KRY_OK otherwise, or when
+ * the store was created without guards. */
+int kry_store_check_guards(kry_store* st);
 
 /* ---- restart-loop pieces (gmres.hpp:100-185), host arithmetic ------------- */
 /* H ((k+1)×k, col-major) from the store's R and records (assemble_hessenberg). */

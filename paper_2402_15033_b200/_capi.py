@@ -90,6 +90,7 @@ SIGNATURES = {
     "kry_operator_rows": (C.c_int, [vp, P_i64, P_i64, P_i64]),
     "kry_operator_nnz": (C.c_int, [vp, P_i64]),
     "kry_operator_jacobi": (C.c_int, [vp]),
+    "kry_store_check_guards": (C.c_int, [vp]),
     "kry_operator_is_jacobi": (C.c_int, [vp, C.POINTER(C.c_int)]),
     "kry_gen_random_sparse": (C.c_int, [i64, i64, i64, i64, C.c_uint64, dbl, C.c_int, P_i64, P_i64, P_dbl]),
     "kry_spmv": (C.c_int, [vp, vp, P_dbl, P_dbl]),

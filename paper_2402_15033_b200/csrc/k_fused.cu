@@ -85,14 +85,15 @@ struct FusedMaps {
 //
 // Tile order of gram_kernel<1, NB, NX>: (jb = 0, ib = 0..NB−1), then the
 // extra tiles (k, ib = 1..NB−1).
-template <int S, int WMAX, int NB, int NX>
+template <int S, int WMAX, int NB, int NX, int CL>
 __global__ void __launch_bounds__(kFuThreads, 1)
     fused_pass_kernel(const __grid_constant__ FusedMaps maps, const FusedPassArgs a, int nslots) {
     KB_PDL_WAIT();
-    if (a.skip && *a.skip) return;  // block j's factorisation failed: nothing may change (k_pip.cu)
+    if (a.skip && *a.skip) return;  // block j's factorisation failed: nothing may change (k_pip.cu); grid-uniform
     constexpr int H = (S + 1) & ~1, STEP = 64 - 2 * H;
     static_assert(STEP % 4 == 0, "core columns must split into 4-row DMMA chunks");
     static_assert(WMAX == S + 1, "the raw block is the MPK block");
+    static_assert(kQR % kFuU == 0 && kGR % kFuG == 0, "rings must be multiples of the role warps");
     constexpr int T = NB + NX * (NB - 1);
     extern __shared__ __align__(1024) unsigned char smem[];
     const int cp = a.c0;
@@ -104,48 +105,65 @@ __global__ void __launch_bounds__(kFuThreads, 1)
     const int nbar = 2 * nslots;
     uint64_t* lfull = reinterpret_cast<uint64_t*>(ring + ring_doubles);  // [2·kMaxSlots]
     uint64_t* lfree = lfull + 2 * kMaxSlots;                             // [2·kMaxSlots]
-    uint64_t* qfull = lfree + 2 * kMaxSlots;
-    uint64_t* qempty = qfull + kQR;
-    uint64_t* gready = qempty + kQR;
-    uint64_t* gempty = gready + kGR;
-    double2* qring = reinterpret_cast<double2*>(gempty + kGR);  // [kQR][32]
-    double* c_sm = reinterpret_cast<double*>(qring + kQR * 32);  // −R_col [cp][WMAX], −R_jj, 1/r_jj
+    uint64_t* qfull = lfree + 2 * kMaxSlots;  // [CL][kQR]  (CTA 0: one ring per writing CTA)
+    uint64_t* qempty = qfull + CL * kQR;      // [kQR]      (this CTA's q slots in CTA 0's ring)
+    uint64_t* gready = qempty + kQR;          // [kGR]      (this CTA's Gram lines)
+    uint64_t* gempty = gready + kGR;          // [CL][kGR]  (CTA 0: per Gram-owning CTA)
+    double2* qring = reinterpret_cast<double2*>(gempty + CL * kGR);  // [CL][kQR][32] (CTA 0)
+    double* c_sm = reinterpret_cast<double*>(qring + CL * kQR * 32);  // −R_col [cp][WMAX], −R_jj, 1/r_jj
     for (int i = threadIdx.x; i < (cp + WMAX + 1) * WMAX; i += blockDim.x) c_sm[i] = a.coef[i];
     if (threadIdx.x == 0) {
         for (int i = 0; i < 2 * kMaxSlots; ++i) {
             mbar_init(&lfull[i], 1);
             mbar_init(&lfree[i], 1);
         }
-        for (int i = 0; i < kQR; ++i) {
-            mbar_init(&qfull[i], 1);
-            mbar_init(&qempty[i], 1);
-        }
-        for (int i = 0; i < kGR; ++i) {
-            mbar_init(&gready[i], 1);
-            mbar_init(&gempty[i], 1);
-        }
+        for (int i = 0; i < CL * kQR; ++i) mbar_init(&qfull[i], 1);
+        for (int i = 0; i < kQR; ++i) mbar_init(&qempty[i], 1);
+        for (int i = 0; i < kGR; ++i) mbar_init(&gready[i], 1);
+        for (int i = 0; i < CL * kGR; ++i) mbar_init(&gempty[i], 1);
         asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
     }
     __syncthreads();
+    if constexpr (CL > 1) cluster_sync_all();  // peers' barriers initialised before any remote arrive
+
+    // Cross-CTA signalling (CL > 1: the pair shares one window column; CTA 0
+    // runs the MPK wavefront over all lines, CTA r the TMA/update/Gram of the
+    // line steps t ≡ r (mod CL), each line's slot in its owner's shared memory).
+    auto arrive_on = [&](uint64_t* bar, unsigned cta) {
+        if constexpr (CL > 1)
+            mbar_arrive_cluster(bar, cta);
+        else
+            mbar_arrive(bar);
+    };
+    auto wait_on = [&](uint64_t* bar, unsigned parity) {
+        if constexpr (CL > 1)
+            mbar_wait_cluster(bar, parity);
+        else
+            mbar_wait(bar, parity);
+    };
+    const int crank = CL > 1 ? static_cast<int>(cluster_rank()) : 0;
+    const int cid = blockIdx.x / CL, ncl = gridDim.x / CL;
 
     const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
     const int nx = a.nx, ny = a.ny;
     const i64 ld = a.ld, nx64 = nx;
-    // Tasks (window wx, band b) in window-major order, task i on CTA i mod
-    // grid: the CTAs of one round cover whole runs of windows at the same
-    // band, so neighbouring windows pass the same lines at the same time (the
-    // overlapping halo columns hit L2), and bands alternate direction so the
-    // 2S lines recomputed at a band seam are the ones the neighbouring band
+    // Tasks (window wx, band b) in window-major order, task i on cluster i mod
+    // clusters: the clusters of one round cover whole runs of windows at the
+    // same band, so neighbouring windows pass the same lines at the same time
+    // (the overlapping halo columns hit L2), and bands alternate direction so
+    // the 2S lines recomputed at a band seam are the ones the neighbouring band
     // processes at the same moment (both reach the seam at the end).
     auto for_tasks = [&](auto&& body) {
-        for (int task = blockIdx.x; task < a.ntasks; task += gridDim.x) {
+        for (int task = cid; task < a.ntasks; task += ncl) {
             const int wx = task / a.nbands, b = task % a.nbands;
             const int y0 = static_cast<int>(static_cast<i64>(b) * ny / a.nbands);
             const int y1 = static_cast<int>(static_cast<i64>(b + 1) * ny / a.nbands);
             body(wx, y0, y1, (b & 1) != 0);
         }
     };
+    // this CTA's line steps of a task: t = crank, crank + CL, …
+    auto own_count = [&](int steps) { return steps > crank ? (steps - crank + CL - 1) / CL : 0; };
     // line of update step t; levels trail the update by k lines, the Gram by S
     auto step_line = [&](int y0, int y1, bool down, int t) { return down ? y1 - 1 + S - t : y0 - S + t; };
     // Steps t < S and t ≥ len + S are recomputed lines outside the band: no
@@ -154,28 +172,29 @@ __global__ void __launch_bounds__(kFuThreads, 1)
 
     if (warp == kFuProd) {
         // ---- TMA producer: window line of [prefix | raw block j] per slot ---
-        if (lane != 0) return;
-        const unsigned tx = static_cast<unsigned>(cp + WMAX) * kBox * 8;
-        int ub = 0;
-        for_tasks([&](int wx, int y0, int y1, bool down) {
-            const int steps = y1 - y0 + 2 * S;
-            const int ix0 = wx * STEP - H;
-            for (int t = 0; t < steps; ++t) {
-                const int ut = ub + t;
-                if (ut >= nslots) {
-                    const int pt = ut - nslots;  // the line this slot held
-                    mbar_wait(&lfree[pt % nbar], (pt / nbar) & 1);
+        if (lane == 0) {
+            const unsigned tx = static_cast<unsigned>(cp + WMAX) * kBox * 8;
+            int ub = 0;
+            for_tasks([&](int wx, int y0, int y1, bool down) {
+                const int steps = y1 - y0 + 2 * S;
+                const int ix0 = wx * STEP - H;
+                for (int o = 0, n = own_count(steps); o < n; ++o) {
+                    const int t = crank + o * CL, ut = ub + o;
+                    if (ut >= nslots) {
+                        const int pt = ut - nslots;  // the line this slot held
+                        mbar_wait(&lfree[pt % nbar], (pt / nbar) & 1);
+                    }
+                    // rows outside [0, n) (lines off the grid) are zero-filled by TMA
+                    const int row0 = step_line(y0, y1, down, t) * nx + ix0;
+                    double* st = slot_of(ut);
+                    uint64_t* bar = &lfull[ut % nbar];
+                    mbar_expect_tx(bar, tx);
+                    if (cp > 0) tma_load_2d(st, &maps.p, row0, 0, bar);
+                    tma_load_2d(st + voff, &maps.v, row0, 0, bar);
                 }
-                // rows outside [0, n) (lines off the grid) are zero-filled by TMA
-                const int row0 = step_line(y0, y1, down, t) * nx + ix0;
-                double* st = slot_of(ut);
-                uint64_t* bar = &lfull[ut % nbar];
-                mbar_expect_tx(bar, tx);
-                if (cp > 0) tma_load_2d(st, &maps.p, row0, 0, bar);
-                tma_load_2d(st + voff, &maps.v, row0, 0, bar);
-            }
-            ub += steps;
-        });
+                ub += own_count(steps);
+            });
+        }
     } else if (warp < kFuU) {
         // ---- update of block j from the slot (K5's arithmetic, term for term)
         const double* nrc = c_sm;
@@ -187,9 +206,9 @@ __global__ void __launch_bounds__(kFuThreads, 1)
             const int ix = wx * STEP - H + 2 * lane;
             const bool in_grid = ix >= 0 && ix < nx;
             const bool store_lane = in_grid && lane >= H / 2 && lane < 32 - H / 2;
-            const int steps = y1 - y0 + 2 * S;
-            for (int t = ((warp - tb) % kFuU + kFuU) % kFuU; t < steps; t += kFuU) {  // tt ≡ warp (mod kFuU)
-                const int tt = tb + t;
+            const int steps = y1 - y0 + 2 * S, nown = own_count(steps);
+            for (int o = ((warp - tb) % kFuU + kFuU) % kFuU; o < nown; o += kFuU) {  // tt ≡ warp (mod kFuU)
+                const int t = crank + o * CL, tt = tb + o;
                 mbar_wait(&lfull[tt % nbar], (tt / nbar) & 1);
                 double* st = slot_of(tt) + 2 * lane;
                 double acc[WMAX][2];
@@ -231,76 +250,95 @@ __global__ void __launch_bounds__(kFuThreads, 1)
                     // the slot is refilled by TMA (async proxy) once the Gram frees it
                     asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
                 }
+                // q to the MPK warp (CTA 0's ring for this CTA's lines)
                 const int qs = tt % kQR;
                 if (tt >= kQR) mbar_wait(&qempty[qs], ((tt / kQR) - 1) & 1);
-                qring[qs * 32 + lane] = q;
+                double2* qdst = qring + (crank * kQR + qs) * 32 + lane;
+                if constexpr (CL > 1)
+                    st_cluster_f64x2(qdst, 0, q);
+                else
+                    *qdst = q;
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(&qfull[qs]);
+                    arrive_on(&qfull[crank * kQR + qs], 0);
                     if (!in_band) mbar_arrive(&lfree[tt % nbar]);  // recomputed line: no Gram
                 }
             }
-            tb += steps;
+            tb += nown;
         });
+        asm volatile("bar.sync 2, %0;" ::"n"((kFuU + kFuG) * 32));  // the ring is free for the Gram scratch
     } else if (warp == kFuMpk) {
-        // ---- MPK of block j+1: levels 1..S of the q wavefront ---------------
+        // ---- MPK of block j+1 (CTA 0): levels 1..S of the q wavefront --------
         // A[k], B[k], C[k]: level k at lines l − k, l − k − 1, l − k − 2 after step l.
-        int tb = 0, gb = 0;
-        for_tasks([&](int wx, int y0, int y1, bool down) {
-            const int ix = wx * STEP - H + 2 * lane;
-            const bool in_grid = ix >= 0 && ix < nx;
-            const bool store_lane = in_grid && lane >= H / 2 && lane < 32 - H / 2;
-            double2 A[S + 1], B[S + 1], C[S + 1];
+        if (crank == 0) {
+            int cq[CL], cg[CL];  // per owning CTA: q lines received, Gram lines signalled
 #pragma unroll
-            for (int k = 0; k <= S; ++k) A[k] = B[k] = C[k] = make_double2(0.0, 0.0);
-            const int steps = y1 - y0 + 2 * S;
-            for (int t = 0; t < steps; ++t) {
-                const int tt = tb + t, slot = tt % kQR;
-                mbar_wait(&qfull[slot], (tt / kQR) & 1);
-                const double2 in = qring[slot * 32 + lane];
-                __syncwarp();
-                if (lane == 0) mbar_arrive(&qempty[slot]);
-                const int l = step_line(y0, y1, down, t);
-                C[0] = B[0];
-                B[0] = A[0];
-                A[0] = in;
+            for (int r = 0; r < CL; ++r) cq[r] = cg[r] = 0;
+            for_tasks([&](int wx, int y0, int y1, bool down) {
+                const int ix = wx * STEP - H + 2 * lane;
+                const bool in_grid = ix >= 0 && ix < nx;
+                const bool store_lane = in_grid && lane >= H / 2 && lane < 32 - H / 2;
+                double2 A[S + 1], B[S + 1], C[S + 1];
 #pragma unroll
-                for (int k = 1; k <= S; ++k) {
-                    // ascending: A = line lk + 1, C = lk − 1; descending: the reverse
-                    const double2 dn = down ? A[k - 1] : C[k - 1], cu = B[k - 1], up = down ? C[k - 1] : A[k - 1];
-                    const double left = __shfl_up_sync(0xffffffffu, cu.y, 1);
-                    const double right = __shfl_down_sync(0xffffffffu, cu.x, 1);
-                    // spmv's stored order: row−nx, row−1, row, row+1, row+nx (K2f)
-                    double s0 = __dadd_rn(0.0, -dn.x);
-                    s0 = __dadd_rn(s0, -left);
-                    s0 = __dadd_rn(s0, __dmul_rn(4.0, cu.x));
-                    s0 = __dadd_rn(s0, -cu.y);
-                    s0 = __dadd_rn(s0, -up.x);
-                    double s1 = __dadd_rn(0.0, -dn.y);
-                    s1 = __dadd_rn(s1, -cu.x);
-                    s1 = __dadd_rn(s1, __dmul_rn(4.0, cu.y));
-                    s1 = __dadd_rn(s1, -right);
-                    s1 = __dadd_rn(s1, -up.y);
-                    const int lk = down ? l + k : l - k;
-                    const bool live = in_grid && lk >= 0 && lk < ny;
-                    const double2 v = live ? make_double2(s0, s1) : make_double2(0.0, 0.0);
-                    C[k] = B[k];
-                    B[k] = A[k];
-                    A[k] = v;
-                    if (store_lane && lk >= y0 && lk < y1)
-                        *reinterpret_cast<double2*>(a.Vn + k * ld + static_cast<i64>(lk) * nx64 + ix) = v;
-                }
-                const int g = t - 2 * S;  // the segment's g-th line (l ∓ S) is complete
-                if (g >= 0 && g < y1 - y0) {
-                    const int gg = gb + g, gs = gg % kGR;
-                    if (gg >= kGR) mbar_wait(&gempty[gs], ((gg / kGR) - 1) & 1);
+                for (int k = 0; k <= S; ++k) A[k] = B[k] = C[k] = make_double2(0.0, 0.0);
+                const int steps = y1 - y0 + 2 * S;
+                for (int t = 0; t < steps; ++t) {
+                    // q of step t from its owner's ring
+                    const int r = t % CL;
+                    int c = 0;
+#pragma unroll
+                    for (int rr = 0; rr < CL; ++rr)
+                        if (rr == r) c = cq[rr]++;
+                    const int qs = c % kQR;
+                    wait_on(&qfull[r * kQR + qs], (c / kQR) & 1);
+                    const double2 in = qring[(r * kQR + qs) * 32 + lane];
                     __syncwarp();
-                    if (lane == 0) mbar_arrive(&gready[gs]);
+                    if (lane == 0) arrive_on(&qempty[qs], r);
+                    const int l = step_line(y0, y1, down, t);
+                    C[0] = B[0];
+                    B[0] = A[0];
+                    A[0] = in;
+#pragma unroll
+                    for (int k = 1; k <= S; ++k) {
+                        // ascending: A = line lk + 1, C = lk − 1; descending: the reverse
+                        const double2 dn = down ? A[k - 1] : C[k - 1], cu = B[k - 1], up = down ? C[k - 1] : A[k - 1];
+                        const double left = __shfl_up_sync(0xffffffffu, cu.y, 1);
+                        const double right = __shfl_down_sync(0xffffffffu, cu.x, 1);
+                        // spmv's stored order: row−nx, row−1, row, row+1, row+nx (K2f)
+                        double s0 = __dadd_rn(0.0, -dn.x);
+                        s0 = __dadd_rn(s0, -left);
+                        s0 = __dadd_rn(s0, __dmul_rn(4.0, cu.x));
+                        s0 = __dadd_rn(s0, -cu.y);
+                        s0 = __dadd_rn(s0, -up.x);
+                        double s1 = __dadd_rn(0.0, -dn.y);
+                        s1 = __dadd_rn(s1, -cu.x);
+                        s1 = __dadd_rn(s1, __dmul_rn(4.0, cu.y));
+                        s1 = __dadd_rn(s1, -right);
+                        s1 = __dadd_rn(s1, -up.y);
+                        const int lk = down ? l + k : l - k;
+                        const bool live = in_grid && lk >= 0 && lk < ny;
+                        const double2 v = live ? make_double2(s0, s1) : make_double2(0.0, 0.0);
+                        C[k] = B[k];
+                        B[k] = A[k];
+                        A[k] = v;
+                        if (store_lane && lk >= y0 && lk < y1)
+                            *reinterpret_cast<double2*>(a.Vn + k * ld + static_cast<i64>(lk) * nx64 + ix) = v;
+                    }
+                    const int g = t - 2 * S;  // the segment's g-th line (l ∓ S) is complete
+                    if (g >= 0 && g < y1 - y0) {
+                        const int owner = (g + S) % CL;  // the CTA that updated line g holds its slot
+                        int cgo = 0;
+#pragma unroll
+                        for (int rr = 0; rr < CL; ++rr)
+                            if (rr == owner) cgo = cg[rr]++;
+                        const int gs = cgo % kGR;
+                        if (cgo >= kGR) mbar_wait(&gempty[owner * kGR + gs], ((cgo / kGR) - 1) & 1);
+                        __syncwarp();
+                        if (lane == 0) arrive_on(&gready[gs], owner);
+                    }
                 }
-            }
-            tb += steps;
-            gb += y1 - y0;
-        });
+            });
+        }
     } else {
         // ---- Gram of block j+1: [V_{j+1} | Q[:, 0:c0']]ᵀ·V_{j+1} --------------
         const int gw = warp - kFuG0;
@@ -320,14 +358,16 @@ __global__ void __launch_bounds__(kFuThreads, 1)
         const int c0n = a.c0n;
         const double* lev = a.Vn + m * ld;
         const bool lev_on = m >= 1 && m < a.w;
-        int gb = 0, tb = 0;
+        int gb = 0, tb = 0;  // this CTA's Gram lines / line steps of the previous tasks
         for_tasks([&](int wx, int y0, int y1, bool down) {
             const int len = y1 - y0;
-            for (int g = ((gw - gb) % kFuG + kFuG) % kFuG; g < len; g += kFuG) {  // gg ≡ gw (mod kFuG)
-                const int gg = gb + g, gs = gg % kGR;
-                mbar_wait(&gready[gs], (gg / kGR) & 1);
+            const int g0 = ((crank - S) % CL + CL) % CL;  // first in-band line whose update step is ours
+            const int gown = len > g0 ? (len - g0 + CL - 1) / CL : 0;
+            for (int k = ((gw - gb) % kFuG + kFuG) % kFuG; k < gown; k += kFuG) {  // gg ≡ gw (mod kFuG)
+                const int g = g0 + k * CL, gg = gb + k, gs = gg % kGR;
+                wait_on(&gready[gs], (gg / kGR) & 1);
                 const int line = down ? y1 - 1 - g : y0 + g;
-                const int tt = tb + g + S;  // update step of this line
+                const int tt = tb + (g + S - crank) / CL;  // this CTA's slot of the line's update step
                 const double* st = slot_of(tt) + H + kq;  // core rows start at slot row H
                 const int cbase = wx * STEP + kq;
                 const i64 rbase = static_cast<i64>(line) * nx64 + cbase;
@@ -350,30 +390,30 @@ __global__ void __launch_bounds__(kFuThreads, 1)
                     for (int ib = 0; ib < NB; ++ib) dmma(acc[ib][0], acc[ib][1], f[ib], f[0]);
                     if constexpr (NX > 0) {
 #pragma unroll
-                        for (int k = 0; k < NX; ++k) {
-                            const int xb = a.xb0 + k;
+                        for (int k2 = 0; k2 < NX; ++k2) {
+                            const int xb = a.xb0 + k2;
                             double fx = 0.0;
 #pragma unroll
                             for (int b = 1; b < NB; ++b)
                                 if (b == xb) fx = f[b];
 #pragma unroll
                             for (int ib = 1; ib < NB; ++ib)
-                                if (ib <= xb) dmma(accx[k][ib][0], accx[k][ib][1], f[ib], fx);
+                                if (ib <= xb) dmma(accx[k2][ib][0], accx[k2][ib][1], f[ib], fx);
                         }
                     }
                 }
                 __syncwarp();
                 if (lane == 0) {
-                    mbar_arrive(&gempty[gs]);
+                    arrive_on(&gempty[crank * kGR + gs], 0);
                     mbar_arrive(&lfree[tt % nbar]);
                 }
             }
-            gb += len;
-            tb += len + 2 * S;
+            gb += gown;
+            tb += own_count(len + 2 * S);
         });
         // cross-warp sums in fixed warp order (K3's packed tile layout), through
-        // the update ring: idle once the last Gram line is ready
-        asm volatile("bar.sync 1, %0;" ::"n"(kFuG * 32));
+        // the update ring: free once this CTA's update warps are done (bar 2)
+        asm volatile("bar.sync 2, %0;" ::"n"((kFuU + kFuG) * 32));
         double* scratch = ring;
         const int e0 = (lane >> 2) + 8 * (2 * (lane & 3));
 #pragma unroll
@@ -402,27 +442,44 @@ __global__ void __launch_bounds__(kFuThreads, 1)
             out[e] = sum;
         }
     }
+    // no CTA of a cluster leaves while a peer may still arrive on its barriers
+    // or write its q ring
+    if constexpr (CL > 1) cluster_sync_all();
 }
 
-template <int S, int WMAX, int NB>
+template <int S, int WMAX, int NB, int CL>
 const void* fused_fn_nb(int nb, int nx) {
     if (nb == NB) {
-        if (nx == 0) return reinterpret_cast<const void*>(fused_pass_kernel<S, WMAX, NB, 0>);
+        if (nx == 0) return reinterpret_cast<const void*>(fused_pass_kernel<S, WMAX, NB, 0, CL>);
         if constexpr (NB > 1) {
-            if (nx == 1) return reinterpret_cast<const void*>(fused_pass_kernel<S, WMAX, NB, 1>);
-            if (nx == 2) return reinterpret_cast<const void*>(fused_pass_kernel<S, WMAX, NB, 2>);
+            if (nx == 1) return reinterpret_cast<const void*>(fused_pass_kernel<S, WMAX, NB, 1, CL>);
+            if (nx == 2) return reinterpret_cast<const void*>(fused_pass_kernel<S, WMAX, NB, 2, CL>);
         }
         return nullptr;
     }
-    if constexpr (NB < 8) return fused_fn_nb<S, WMAX, NB + 1>(nb, nx);
+    if constexpr (NB < 8) return fused_fn_nb<S, WMAX, NB + 1, CL>(nb, nx);
     return nullptr;
 }
 
 constexpr size_t kFuSmem = 225 * 1024;
 size_t fused_slot_bytes(i64 c0) { return static_cast<size_t>(round_up(c0 * kBox, 16) + round_up(6 * kBox, 16)) * 8; }
+constexpr int kMaxCl = 2;  // cluster size of the paired variant
 size_t fused_fixed_smem(i64 c0) {
-    return static_cast<size_t>(4 * kMaxSlots + 2 * kQR + 2 * kGR) * 8 + static_cast<size_t>(kQR) * 32 * 16 +
-           static_cast<size_t>(c0 + 7) * 6 * 8;
+    return static_cast<size_t>(4 * kMaxSlots + (kMaxCl + 1) * kQR + (kMaxCl + 1) * kGR) * 8 +
+           static_cast<size_t>(kMaxCl * kQR) * 32 * 16 + static_cast<size_t>(c0 + 7) * 6 * 8;
+}
+// KRY_FUSED_CLUSTER=2: a CTA pair (thread-block cluster) per window column,
+// the line slots split between the two SMs' shared memory (2× the lines in
+// flight), q and the Gram-ready signals crossing the pair through DSMEM and
+// cluster-scope mbarriers.  Parity-green but measured far slower than one CTA
+// per window (4000²: 88.1 vs 34.6 ms per cycle; 8000²: 342 vs 135 ms): every
+// line step now waits on a cross-SM handoff.  Default 1.
+int fused_cluster() {
+    static const int cl = [] {
+        const char* e = std::getenv("KRY_FUSED_CLUSTER");
+        return e && std::atoi(e) == 2 ? 2 : 1;
+    }();
+    return cl;
 }
 
 }  // namespace
@@ -452,13 +509,14 @@ void launch_fused_pass(cudaStream_t stream, const StencilGeom& g, int s, FusedPa
     } else {
         a.xb0 = 0;
     }
-    const void* fn = s == 5 ? fused_fn_nb<5, 6, 1>(nb, nxt) : nullptr;
+    const int CL = fused_cluster();
+    const void* fn = s != 5 ? nullptr : CL == 2 ? fused_fn_nb<5, 6, 1, 2>(nb, nxt) : fused_fn_nb<5, 6, 1, 1>(nb, nxt);
     if (!fn) fail(KRY_UNSUPPORTED, "fused pass shape");
     a.nx = static_cast<int>(g.nx);
     a.ny = static_cast<int>(g.ny);
     const i64 nwx = ceil_div(g.nx, step);
-    const i64 sms = device_sms();
-    // bands per window: minimise rounds × (band + 2S) line steps per CTA
+    const i64 sms = device_sms() / CL;  // clusters (one window column each)
+    // bands per window: minimise rounds × (band + 2S) line steps per cluster
     {
         i64 best = -1, best_cost = 0;
         for (i64 nb = 1; nb <= std::max<i64>(1, g.ny / (4 * s)) && nb <= 4096; ++nb) {
@@ -487,10 +545,26 @@ void launch_fused_pass(cudaStream_t stream, const StencilGeom& g, int s, FusedPa
     const size_t ring = std::max(static_cast<size_t>(nslots) * slot_bytes, static_cast<size_t>(kFuG) * T * 64 * 8);
     const size_t smem = ring + fixed;
     set_kernel_smem(fn, smem);
-    const int grid = static_cast<int>(std::max<i64>(1, std::min<i64>(sms, a.ntasks)));
+    const int grid = CL * static_cast<int>(std::max<i64>(1, std::min<i64>(sms, a.ntasks)));
     if (static_cast<i64>(grid) * T * 64 > fused_partials_doubles()) fail(KRY_INTERNAL, "fused pass partials");
     void* args[] = {&maps, &a, &nslots};
-    launch_pdl_c(fn, dim3(grid), dim3(kFuThreads), smem, stream, args);
+    if (!launches_suppressed()) {
+        cudaLaunchConfig_t cfg{};
+        cfg.gridDim = dim3(grid);
+        cfg.blockDim = dim3(kFuThreads);
+        cfg.dynamicSmemBytes = smem;
+        cfg.stream = stream;
+        cudaLaunchAttribute at[2];
+        at[0].id = cudaLaunchAttributeProgrammaticStreamSerialization;
+        at[0].val.programmaticStreamSerializationAllowed = pdl_enabled() ? 1 : 0;
+        at[1].id = cudaLaunchAttributeClusterDimension;
+        at[1].val.clusterDim.x = CL;
+        at[1].val.clusterDim.y = 1;
+        at[1].val.clusterDim.z = 1;
+        cfg.attrs = at;
+        cfg.numAttrs = 2;
+        KB_CUDA(cudaLaunchKernelExC(&cfg, fn, args));
+    }
     KB_LAUNCHED();
     launch_gram_reduce(stream, a.partials, grid, T * 64, d_packed);
     launches += 2;

@@ -711,6 +711,10 @@ int kry_store_block_record(kry_store* st, int64_t index, int64_t* c0, int64_t* w
     });
 }
 
+int kry_store_check_guards(kry_store* st) {
+    return guarded([&] { st->st->check_guards(); });
+}
+
 int kry_store_device_ptr(kry_store* st, double** d_q, int64_t* ld) {
     return guarded([&] {
         *d_q = st->st->col(0);

@@ -171,6 +171,11 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
         return rep;
     }
 
+    {
+        const char* e = std::getenv("KRY_GUARD");
+        const bool want_guard = e && std::atoi(e) == 1;
+        if (W.store && W.store->guarded() != want_guard) W.store.reset();
+    }
     if (!W.store) W.store = std::make_unique<Store>(ctx, n, m, s, shat);
     Store& store = *W.store;
     // Small grids: the basis prefix is re-read by every block's Gram and
@@ -572,6 +577,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
         rep.reduces_per_iteration = static_cast<double>(rep.sync.reduces) / static_cast<double>(rep.iterations);
     rep.ortho_bytes = store.ortho_bytes;
     finish();
+    store.check_guards();  // KRY_GUARD debug builds of the basis: no kernel wrote outside it
     if (ctx.host_profile) {
         const double wall = std::chrono::duration<double>(std::chrono::steady_clock::now() - prof_t0).count();
         std::fprintf(stderr,

@@ -26,8 +26,37 @@ Store::Store(Ctx& ctx, i64 n, i64 m, i64 panel_size, i64 big_panel_size)
     pgram_ = Mat(max_cols_, max_cols_);
     pready_.assign(static_cast<size_t>(max_cols_), 0);
     if (const char* e = std::getenv("KRY_FUSED_PANEL_GRAM")) fused_panel_gram_ = std::atoi(e) != 0;
-    q_.ensure(static_cast<size_t>(ld_) * max_cols_ * 8);
-    KB_CUDA(cudaMemsetAsync(q_.p, 0, static_cast<size_t>(ld_) * max_cols_ * 8, ctx_.stream));
+    if (const char* e = std::getenv("KRY_GUARD")) qoff_ = std::atoi(e) == 1 ? 1 : 0;
+    q_.ensure(static_cast<size_t>(ld_) * (max_cols_ + 2 * qoff_) * 8);
+    zero_q();
+}
+
+void Store::zero_q() {
+    KB_CUDA(cudaMemsetAsync(q_.p, 0, q_.bytes, ctx_.stream));
+    if (guarded()) fill_guards();
+}
+
+void Store::fill_guards() {
+    const size_t colb = static_cast<size_t>(ld_) * 8;
+    KB_CUDA(cudaMemsetAsync(q_.p, 0xFF, colb, ctx_.stream));                           // column −1
+    KB_CUDA(cudaMemsetAsync(q_.p + (max_cols_ + 1) * ld_, 0xFF, colb, ctx_.stream));  // column m + 1
+    if (ld_ > n_)  // padding rows [n, ld) of every column
+        KB_CUDA(cudaMemset2DAsync(col(0) + n_, colb, 0xFF, static_cast<size_t>(ld_ - n_) * 8, max_cols_,
+                                  ctx_.stream));
+}
+
+void Store::check_guards() {
+    if (!guarded()) return;
+    std::vector<uint64_t> h(static_cast<size_t>(ld_) * (max_cols_ + 2));
+    KB_CUDA(cudaMemcpyAsync(h.data(), q_.p, h.size() * 8, cudaMemcpyDeviceToHost, ctx_.stream));
+    ctx_.sync();
+    for (i64 c = 0; c < max_cols_ + 2; ++c) {
+        const bool guard_col = c == 0 || c == max_cols_ + 1;
+        for (i64 r = guard_col ? 0 : n_; r < ld_; ++r)
+            if (h[static_cast<size_t>(c * ld_ + r)] != ~uint64_t(0))
+                fail(KRY_INTERNAL, "KRY_GUARD: basis guard overwritten at column " + std::to_string(c - 1) + ", row " +
+                                       std::to_string(r));
+    }
 }
 
 bool Store::deferred_coefficients(const std::vector<double>& y, std::vector<double>& y_out) const {
@@ -191,7 +220,7 @@ bool Store::can_fuse(const Operator& op, i64 s) {
     if (!on || !can_speculate(s + 1) || op.kind != Operator::LAPLACE2D || ctx_.nranks != 1 || op.nloc != n_) return false;
     for (auto& b : fraw_) b.ensure(static_cast<size_t>(ld_) * (s + 1) * 8);
     ctx_.gram_partials.ensure(static_cast<size_t>(std::max(fused_partials_doubles(), gram_scratch_doubles(s + 1))) * 8);
-    return fused_pass_supported(op.geom, static_cast<int>(s), s + 1, max_cols_ - (s + 1), ld_, q_.p, fraw_[0].p,
+    return fused_pass_supported(op.geom, static_cast<int>(s), s + 1, max_cols_ - (s + 1), ld_, col(0), fraw_[0].p,
                                 fraw_[1].p);
 }
 
@@ -224,7 +253,7 @@ void Store::spec_fused_next(Operator& op, i64 s) {
     const SpecPlan p = spec_plan(w, true);
     const int nbuf = 1 - fpend_.buf;
     FusedPassArgs f{};
-    f.Q = q_.p;
+    f.Q = col(0);
     f.ld = ld_;
     f.V = fraw_[fpend_.buf].p;
     f.Vn = fraw_[nbuf].p;

@@ -47,13 +47,21 @@ public:
     const Upper& coefficients() const { return r_; }
     const std::vector<int>& panel_states() const { return states_; }
     const std::vector<BlockRecord>& block_records() const { return records_; }
-    double* col(i64 j) { return q_.p + j * ld_; }
-    const double* col(i64 j) const { return q_.p + j * ld_; }
+    double* col(i64 j) { return q_.p + (j + qoff_) * ld_; }
+    const double* col(i64 j) const { return q_.p + (j + qoff_) * ld_; }
+    // KRY_GUARD=1 (debug, read at construction): the basis is allocated with a
+    // guard column on each side, and the guard columns and every column's
+    // padding rows [n, ld) hold an all-ones NaN pattern that no kernel may
+    // write (and none may read without poisoning its result) — an
+    // out-of-bounds check of every kernel that touches the store, for a pool
+    // where compute-sanitizer is unavailable.  check_guards() fails loudly.
+    bool guarded() const { return qoff_ != 0; }
+    void check_guards();
     i64 ld() const { return ld_; }
     Ctx& ctx() { return ctx_; }
 
     void reset();
-    void zero_q() { KB_CUDA(cudaMemsetAsync(q_.p, 0, q_.bytes, ctx_.stream)); }
+    void zero_q();
     void seed_unit_column(const double* d_v);
     // V (device, n×w, leading dimension ldv) may be the store's own columns
     // [c0, c0+w) (in-place path used by the solver's MPK) or a caller buffer.
@@ -184,6 +192,8 @@ private:
     i64 filled_ = 0, finalized_ = 0, big_panel_start_ = 0;
     bool seam_valid_ = false;
     DevBuf q_;
+    i64 qoff_ = 0;  // 1 with guard columns (KRY_GUARD)
+    void fill_guards();
     i64 ld_;
     Upper r_;
     std::vector<int> states_;

@@ -29,7 +29,7 @@ def load(path):
 def family(name):
     if name.startswith("gram_kernel"):
         return "gram_kernel"
-    if name.startswith("update_kernel"):
+    if name.startswith("update_"):  # update_kernel, update_tma_kernel, update_mma_kernel
         return "update_kernel"
     return name
 
@@ -64,8 +64,16 @@ def main():
         out["_source"] = (f"{a.csv} (ncu --metrics gpu__time_duration.sum,dram__bytes_read.sum,dram__bytes_write.sum "
                           "--clock-control none over `bench.py --steps 1 --warmup 1 --no-cpu-baseline --no-e2e "
                           "--no-tts512`); mean DRAM bytes per launch of the family over the timed restart cycle")
+        try:
+            old = json.load(open(a.traffic_out))
+        except (OSError, ValueError):
+            old = {}
+        src = old.pop("_source", None)
+        old.update(out)
+        if src and src != out["_source"]:
+            old["_source"] = f"{out['_source']}; earlier keys: {src}"
         with open(a.traffic_out, "w") as f:
-            json.dump(out, f, indent=1)
+            json.dump(old, f, indent=1)
         print(json.dumps(out, indent=1))
 
 

@@ -34,14 +34,64 @@ Ctx::Ctx(int dev, int nr, int rk, const void* nccl_id) : device(dev), nranks(nr)
         ncclUniqueId id;
         std::memcpy(&id, nccl_id, sizeof(id));
         KB_NCCL(ncclCommInitRank(&comm, nranks, id, rank));
+        const char* e = std::getenv("KRY_PEER_ALLREDUCE");
+        if (!(e && std::atoi(e) == 0) && nranks <= kPeerMaxRanks) setup_peer();
     }
     partials.ensure(static_cast<size_t>(reduce_grid() + 64) * 8);
     h_scalar.ensure(64 * 8);
 }
 
+void Ctx::setup_peer() {
+    // Receive area + flags of this rank, exported through CUDA IPC; every
+    // rank maps every peer's (one collective exchange of the handles).
+    peer_data.ensure(static_cast<size_t>(2) * nranks * kPeerMaxDoubles * 8);
+    peer_flags.ensure(static_cast<size_t>(2) * nranks * 8);
+    KB_CUDA(cudaMemset(peer_flags.p, 0, static_cast<size_t>(2) * nranks * 8));
+    cudaIpcMemHandle_t mine[2];
+    KB_CUDA(cudaIpcGetMemHandle(&mine[0], peer_data.p));
+    KB_CUDA(cudaIpcGetMemHandle(&mine[1], peer_flags.p));
+    const size_t hb = sizeof(mine);
+    DevBuf d;
+    d.ensure(hb * nranks);
+    KB_CUDA(cudaMemcpy(reinterpret_cast<char*>(d.p) + hb * rank, mine, hb, cudaMemcpyHostToDevice));
+    KB_NCCL(ncclAllGather(reinterpret_cast<char*>(d.p) + hb * rank, d.p, hb, ncclChar, comm, stream));
+    std::vector<cudaIpcMemHandle_t> all(2 * static_cast<size_t>(nranks));
+    KB_CUDA(cudaMemcpyAsync(all.data(), d.p, hb * nranks, cudaMemcpyDeviceToHost, stream));
+    KB_CUDA(cudaStreamSynchronize(stream));
+    auto* t = new PeerTable{};
+    for (int r = 0; r < nranks; ++r) {
+        if (r == rank) {
+            t->data[r] = peer_data.p;
+            t->flags[r] = peer_flags.as<uint64_t>();
+            continue;
+        }
+        void* pd = nullptr;
+        void* pf = nullptr;
+        if (cudaIpcOpenMemHandle(&pd, all[2 * r], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess ||
+            cudaIpcOpenMemHandle(&pf, all[2 * r + 1], cudaIpcMemLazyEnablePeerAccess) != cudaSuccess) {
+            // no peer mapping on this system: every rank must agree, so fail
+            // loudly rather than mix the two reduction paths
+            cudaGetLastError();
+            delete t;
+            fail(KRY_CUDA_ERROR, "peer allreduce: cudaIpcOpenMemHandle failed (set KRY_PEER_ALLREDUCE=0)");
+        }
+        peer_opened.push_back(pd);
+        peer_opened.push_back(pf);
+        t->data[r] = static_cast<double*>(pd);
+        t->flags[r] = static_cast<uint64_t*>(pf);
+    }
+    peer_table = t;
+    peer = true;
+    // every rank has mapped every peer before the first peer store
+    KB_NCCL(ncclAllReduce(d.p, d.p, 1, ncclChar, ncclSum, comm, stream));
+    KB_CUDA(cudaStreamSynchronize(stream));
+}
+
 Ctx::~Ctx() {
     cudaSetDevice(device);
     if (stream) cudaStreamSynchronize(stream);
+    for (void* p : peer_opened) cudaIpcCloseMemHandle(p);
+    delete static_cast<PeerTable*>(peer_table);
     for (auto& p : pending) {
         pool.push_back(p.a);
         pool.push_back(p.b);
@@ -121,7 +171,12 @@ void Ctx::resolve_timers() {
 
 void Ctx::allreduce_sum(double* d, size_t count) {
     if (nranks <= 1 || count == 0) return;
-    KB_NCCL(ncclAllReduce(d, d, count, ncclDouble, ncclSum, comm, stream));
+    if (peer && count <= static_cast<size_t>(kPeerMaxDoubles)) {
+        launch_peer_allreduce(stream, d, static_cast<int>(count), *static_cast<const PeerTable*>(peer_table), rank,
+                              nranks, ++peer_epoch, launches);
+    } else {
+        KB_NCCL(ncclAllReduce(d, d, count, ncclDouble, ncclSum, comm, stream));
+    }
     ++allreduces;
 }
 

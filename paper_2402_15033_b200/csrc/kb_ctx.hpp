@@ -108,8 +108,16 @@ struct Ctx {
     void resolve_timers();  // after a stream sync: accumulate elapsed times
     void drain_timers();    // accumulate the phases that already finished (no wait)
 
-    // Σ over ranks, in place on the device (no-op for one rank).
+    // Σ over ranks, in place on the device (no-op for one rank): the
+    // one-shot peer-memory allreduce (k_peer.cu) when the context mapped its
+    // peers (KRY_PEER_ALLREDUCE, default on), else ncclAllReduce.
     void allreduce_sum(double* d, size_t count);
+    bool peer = false;
+    DevBuf peer_data, peer_flags;         // this rank's receive area and flags
+    std::vector<void*> peer_opened;       // peers' areas mapped through CUDA IPC
+    uint64_t peer_epoch = 0;
+    void* peer_table = nullptr;           // PeerTable (host copy, kernel argument)
+    void setup_peer();
     // Device scalar sum of r² style partials → host value (allreduced).
     double finalize_scalar(const double* d_partials, int count);
 };

@@ -106,6 +106,16 @@ int launch_csr_sliced(cudaStream_t s, i64 nloc, int nslices, const int32_t* cons
                       const int32_t* const* col, const double* const* vals, const double* x, const double* b,
                       double* y, double* partials, double* part_sum, int64_t& launches);
 int reduce_grid();  // fixed grid of every partial-sum kernel (determinism)
+
+// ---- k_peer.cu : one-shot deterministic allreduce over NVLink peer memory --
+constexpr int kPeerMaxRanks = 8;
+constexpr int kPeerMaxDoubles = 16384;  // per slot (the widest packed Gram is ~2.3 K doubles)
+struct PeerTable {
+    double* data[kPeerMaxRanks];   // each rank's receive area [2][nranks][kPeerMaxDoubles]
+    uint64_t* flags[kPeerMaxRanks];  // each rank's flags [2][nranks]
+};
+void launch_peer_allreduce(cudaStream_t s, double* d, int count, const PeerTable& t, int rank, int nranks,
+                           uint64_t epoch, int64_t& launches);
 // Jacobi (D⁻¹A formed in place on the device; D⁻¹b per solve).  One of
 // rp64 / rp32 is non-null (unsliced CSR / one column slice).
 void launch_csr_find_diag(cudaStream_t s, i64 nloc, const int64_t* rp64, const int32_t* rp32, const int32_t* col,

@@ -2,7 +2,8 @@
 
 Launches tests/dist_parity.py with torchrun at N = 2 (and N = 4 when four
 GPUs are visible): row-partitioned solves with NCCL halos and one Gram
-allreduce per BCGS-PIP must match the reference's golden reports."""
+allreduce per BCGS-PIP must match the reference's golden reports — through
+the one-shot NVLink peer-memory allreduce (default) and through NCCL."""
 import json
 import os
 import socket
@@ -23,8 +24,9 @@ def free_port():
     return p
 
 
+@pytest.mark.parametrize("peer", ["1", "0"])  # one-shot NVLink peer allreduce (k_peer.cu) / ncclAllReduce
 @pytest.mark.parametrize("nranks", [2, 4])
-def test_row_partitioned_solves_match_reference(kb, nranks, tmp_path):
+def test_row_partitioned_solves_match_reference(kb, nranks, peer, tmp_path):
     if kb.device_count() < nranks:
         pytest.skip(f"needs {nranks} GPUs")
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={nranks}",
@@ -33,7 +35,7 @@ def test_row_partitioned_solves_match_reference(kb, nranks, tmp_path):
     out_dir = tmp_path / "ranks"
     out_dir.mkdir()
     p = subprocess.run(cmd, capture_output=True, text=True, timeout=900, cwd=ROOT,
-                       env={**os.environ, "KRY_DIST_OUT": str(out_dir)})
+                       env={**os.environ, "KRY_DIST_OUT": str(out_dir), "KRY_PEER_ALLREDUCE": peer})
     assert p.returncode == 0, (p.stdout[-3000:], p.stderr[-3000:])
     lines = [json.loads(f.read_text()) for f in sorted(out_dir.glob("rank*.json"))]
     assert len(lines) == nranks and all(l["ok"] for l in lines), lines

@@ -110,7 +110,7 @@ struct Ctx {
 
     // Σ over ranks, in place on the device (no-op for one rank): the
     // one-shot peer-memory allreduce (k_peer.cu) when the context mapped its
-    // peers (KRY_PEER_ALLREDUCE, default on), else ncclAllReduce.
+    // peers (KRY_PEER_ALLREDUCE=1, opt-in), else ncclAllReduce.
     void allreduce_sum(double* d, size_t count);
     bool peer = false;
     DevBuf peer_data, peer_flags;         // this rank's receive area and flags

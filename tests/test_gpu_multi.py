@@ -3,7 +3,7 @@
 Launches tests/dist_parity.py with torchrun at N = 2 (and N = 4 when four
 GPUs are visible): row-partitioned solves with NCCL halos and one Gram
 allreduce per BCGS-PIP must match the reference's golden reports — through
-the one-shot NVLink peer-memory allreduce (default) and through NCCL."""
+NCCL (default) and through the one-shot NVLink peer-memory allreduce."""
 import json
 import os
 import socket

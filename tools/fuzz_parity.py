@@ -19,7 +19,8 @@ for case in range(ncases):
     s = int(rng.integers(1, 9 if wide else 8))
     m = s * int(rng.integers(2, max(3, (129 if wide else 61) // s)))
     shat = 0 if kind != 3 else s * int(rng.integers(1, m // s + 1))
-    opk = rng.choice(["lap2d", "lap3d", "rand"])
+    opk = str(rng.choice(["lap2d", "lap3d", "rand", "gen_jac", "lap_jac"]))
+    jac = None  # Jacobi: the device operator gets kry_operator_jacobi, the reference D⁻¹A and D⁻¹b
     if opk == "lap2d":
         nx, ny = int(rng.integers(2, 70)), int(rng.integers(2, 70))
         a = ref.laplace2d(nx, ny)
@@ -28,6 +29,22 @@ for case in range(ncases):
         d = [int(rng.integers(2, 14)) for _ in range(3)]
         a = ref.laplace3d(*d)
         op = kb.Laplace3D(*d)
+    elif opk == "gen_jac":  # BASELINE configs[4] generator, random size / density / diagonal
+        n = int(rng.integers(10, 20000))
+        per = int(rng.integers(1, min(31, n) + 1))
+        df = float(rng.uniform(0.12, 0.6))
+        rp, ci, vv = kb.gen_random_sparse(n, per_row=per, seed=int(rng.integers(1, 1 << 30)), diag_factor=df)
+        a = ref.Csr(n, rp, ci, vv)
+        op = kb.CsrOperator(rp, ci, vv)
+        jac = vv[ci == np.repeat(np.arange(n), np.diff(rp))]
+    elif opk == "lap_jac":
+        if rng.integers(0, 2):
+            d = [int(rng.integers(2, 70)), int(rng.integers(2, 70))]
+            a, op, dd = ref.laplace2d(*d), kb.Laplace2D(*d), 4.0
+        else:
+            d = [int(rng.integers(2, 14)) for _ in range(3)]
+            a, op, dd = ref.laplace3d(*d), kb.Laplace3D(*d), 6.0
+        jac = np.full(a.n, dd)
     else:
         n = int(rng.integers(5, 3000))
         per = int(rng.integers(0, 12))
@@ -44,6 +61,14 @@ for case in range(ncases):
         a = ref.Csr(n, rp, ci, vv)
         op = kb.CsrOperator(rp, ci, vv)
     b = ref.spmv(a, np.ones(a.n))
+    if jac is not None:  # the reference solves the host pre-scaled system
+        rows = np.repeat(np.arange(a.n), np.diff(a.row_ptr))
+        b_dev = b
+        a = ref.Csr(a.n, a.row_ptr, a.col_idx, a.vals / jac[rows])
+        b = b / jac
+        op.jacobi()
+    else:
+        b_dev = b
     max_iters = m * int(rng.integers(1, 6))
     cfgr = ref.make_config(m=m, s=s, kind=kind, big_step=shat, shat=shat, max_iters=max_iters)
     want = ref.solve(a, b, None, cfgr)
@@ -52,7 +77,7 @@ for case in range(ncases):
     want_fma = ref.solve(a, b, None, cfgr)  # the reference's own rounding envelope (FMA build)
     ref._lib = saved
     try:
-        got = kb.sstep_gmres(op, b, None, kb.SolverConfig(restart_len=m, step=s, big_step=shat,
+        got = kb.sstep_gmres(op, b_dev, None, kb.SolverConfig(restart_len=m, step=s, big_step=shat,
                                                            scheme=kb.OrthoScheme(kb.OrthoKind(kind), shat),
                                                            max_iters=max_iters))
         mine = (int(got.status), got.iterations, got.restarts, got.sync.reduces)

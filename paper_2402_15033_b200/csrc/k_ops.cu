@@ -325,6 +325,110 @@ __global__ void __launch_bounds__(kBlock, 6) stencil3d_vec_kernel(const StencilG
     }
 }
 
+// 3-D 7-point stencil, plane tiles: a CTA of 8 warps owns a 64 × 8 (x × y)
+// tile of grid columns — warp w is tile row w, lane l columns 2l, 2l+1 —
+// and walks kT3Planes planes along z with the planes below / current / above
+// of its own columns in registers (one new 16-byte load per plane from
+// HBM).  The y-neighbours of the tile's interior rows come from a shared
+// copy of the current plane (double-buffered by step parity, one barrier
+// per plane) instead of from L2 (stencil3d_vec_kernel reads every cell three
+// times: as its own value and as both rows' y-neighbour); only the tile's
+// edge rows read their outer neighbour from global memory.  x-neighbours by
+// shuffle.  Same per-row summation order as stencil_kernel<3>
+// (bit-identical).
+constexpr int kT3Rows = 8;
+constexpr int kT3Planes = 16;
+
+template <bool RESID, bool JAC>
+__global__ void __launch_bounds__(kBlock) stencil3d_tile_kernel(const StencilGeom g, const double* __restrict__ x,
+                                                                const double* __restrict__ halo_lo,
+                                                                const double* __restrict__ halo_hi,
+                                                                const double* __restrict__ b,
+                                                                double* __restrict__ y,
+                                                                double* __restrict__ partials) {
+    KB_PDL_WAIT();
+    __shared__ double2 tile[2][kT3Rows][32];
+    const int nx = static_cast<int>(g.nx), ny = static_cast<int>(g.ny);
+    const i64 plane = g.nx * g.ny;
+    const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+    const int ntx = (nx + 63) / 64;
+    const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
+    const int ix = tx * 64 + 2 * lane, iy = ty * kT3Rows + w;
+    const bool active = ix < nx && iy < ny;  // nx even: both columns or neither
+    const bool has_ym = iy > 0, has_yp = iy + 1 < ny, has_l = ix > 0, has_r = ix + 2 < nx;
+    const int off = iy * nx + ix;
+    auto ld2 = [](const double* p) { return *reinterpret_cast<const double2*>(p); };
+    const double c = g.c_off;
+    double sq = 0.0;
+    const int nzl = static_cast<int>(g.nzl), nz = static_cast<int>(g.nz), z0 = static_cast<int>(g.z0);
+    const int zc = blockIdx.y * kT3Planes, zend = min(zc + kT3Planes, nzl);
+    int gz = z0 + zc;
+    const double* xc = x + static_cast<i64>(zc) * plane + off;
+    double* yc = y + static_cast<i64>(zc) * plane + off;
+    const double* bc = RESID ? b + static_cast<i64>(zc) * plane + off : nullptr;
+    double2 down = make_double2(0.0, 0.0), cur = make_double2(0.0, 0.0);
+    if (active && zc < nzl) {
+        if (gz > 0) down = zc > 0 ? ld2(xc - plane) : ld2(halo_lo + off);
+        cur = ld2(xc);
+    }
+    int par = 0;
+#pragma unroll 1
+    for (int l = zc; l < zend; ++l, ++gz, xc += plane, yc += plane) {
+        const bool has_dn = gz > 0, has_up = gz + 1 < nz;
+        double2 up = make_double2(0.0, 0.0);
+        if (active && has_up) up = l + 1 < nzl ? ld2(xc + plane) : ld2(halo_hi + off);
+        tile[par][w][lane] = cur;
+        __syncthreads();
+        double left = __shfl_up_sync(0xffffffffu, cur.y, 1);
+        double right = __shfl_down_sync(0xffffffffu, cur.x, 1);
+        if (active) {
+            if (lane == 0 && has_l) left = xc[-1];
+            if (lane == 31 && has_r) right = xc[2];
+            const double2 ym = !has_ym ? make_double2(0.0, 0.0) : w > 0 ? tile[par][w - 1][lane] : ld2(xc - nx);
+            const double2 yp = !has_yp ? make_double2(0.0, 0.0)
+                                       : w + 1 < kT3Rows ? tile[par][w + 1][lane] : ld2(xc + nx);
+            double s0 = 0.0, s1 = 0.0;
+            if (has_dn) s0 = off_term<JAC>(s0, c, down.x);
+            if (has_ym) s0 = off_term<JAC>(s0, c, ym.x);
+            if (has_l) s0 = off_term<JAC>(s0, c, left);
+            s0 = diag_term<JAC>(s0, 6.0, cur.x);
+            s0 = off_term<JAC>(s0, c, cur.y);
+            if (has_yp) s0 = off_term<JAC>(s0, c, yp.x);
+            if (has_up) s0 = off_term<JAC>(s0, c, up.x);
+            if (has_dn) s1 = off_term<JAC>(s1, c, down.y);
+            if (has_ym) s1 = off_term<JAC>(s1, c, ym.y);
+            s1 = off_term<JAC>(s1, c, cur.x);
+            s1 = diag_term<JAC>(s1, 6.0, cur.y);
+            if (has_r) s1 = off_term<JAC>(s1, c, right);
+            if (has_yp) s1 = off_term<JAC>(s1, c, yp.y);
+            if (has_up) s1 = off_term<JAC>(s1, c, up.y);
+            if (RESID) {
+                const double2 bb = ld2(bc);
+                bc += plane;
+                const double r0 = __dsub_rn(bb.x, s0), r1 = __dsub_rn(bb.y, s1);
+                *reinterpret_cast<double2*>(yc) = make_double2(r0, r1);
+                sq = fma(r0, r0, sq);
+                sq = fma(r1, r1, sq);
+            } else {
+                *reinterpret_cast<double2*>(yc) = make_double2(s0, s1);
+            }
+        }
+        down = cur;
+        cur = up;
+        par ^= 1;
+    }
+    if (RESID) {
+        const double t = block_sum(sq);
+        if (threadIdx.x == 0) partials[blockIdx.y * gridDim.x + blockIdx.x] = t;
+    }
+}
+
+dim3 stencil3d_tile_grid(const StencilGeom& g) {
+    const i64 tiles = ceil_div(g.nx, 64) * ceil_div(g.ny, kT3Rows);
+    const i64 chunks = std::max<i64>(1, ceil_div(g.nzl, kT3Planes));
+    return dim3(static_cast<unsigned>(tiles), static_cast<unsigned>(std::min<i64>(chunks, 65535)));
+}
+
 // K2f: the whole s-step MPK of the 5-point stencil in one pass
 // (mpk_monomial, gmres.hpp:80-90): out[:, k−1] = A^k·x for k = 1..S.
 // Temporal blocking: each warp owns a 64-column window (32 lanes × double2)
@@ -772,8 +876,8 @@ dim3 stencil3d_vec_grid(const StencilGeom& g) {
 }
 
 int stencil_partials(const StencilGeom& g) {
-    const dim3 d = stencil_grid(g), v = stencil3d_vec_grid(g);
-    return static_cast<int>(std::max(d.x * d.y, g.dims == 3 ? v.x * v.y : 0u));
+    const dim3 d = stencil_grid(g), v = stencil3d_vec_grid(g), t = stencil3d_tile_grid(g);
+    return static_cast<int>(std::max({d.x * d.y, g.dims == 3 ? v.x * v.y : 0u, g.dims == 3 ? t.x * t.y : 0u}));
 }
 
 int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const double* halo_lo,
@@ -790,10 +894,23 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
         ++launches;
         return b ? static_cast<int>(grid.x * grid.y) : 0;
     }
-    static const bool vec3 = [] {
+    // KRY_STENCIL3D_VEC: 0 = scalar kernel, 1 = stencil3d_vec_kernel (y-neighbours
+    // from L2), 2 (default) = stencil3d_tile_kernel (y-neighbours from shared memory)
+    static const int vec3 = [] {
         const char* e = std::getenv("KRY_STENCIL3D_VEC");
-        return !e || std::atoi(e) != 0;
+        return e ? std::atoi(e) : 2;
     }();
+    if (vec3 == 2 && g.dims == 3 && (g.nx & 1) == 0 && g.nx * g.ny < (i64(1) << 30) && g.nzl < (i64(1) << 30) &&
+        a16(x) && a16(y) && a16(b) && a16(halo_lo) && a16(halo_hi) && ceil_div(g.nx, 64) * ceil_div(g.ny, kT3Rows) < (i64(1) << 31)) {
+        const dim3 grid = stencil3d_tile_grid(g);
+        if (b)
+            (g.jacobi ? launch_pdl(stencil3d_tile_kernel<true, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials) : launch_pdl(stencil3d_tile_kernel<true, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials));
+        else
+            (g.jacobi ? launch_pdl(stencil3d_tile_kernel<false, true>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials) : launch_pdl(stencil3d_tile_kernel<false, false>, grid, kBlock, 0, s, g, x, halo_lo, halo_hi, b, y, partials));
+        KB_LAUNCHED();
+        ++launches;
+        return b ? static_cast<int>(grid.x * grid.y) : 0;
+    }
     if (vec3 && g.dims == 3 && (g.nx & 1) == 0 && g.nx * g.ny < (i64(1) << 30) && g.nzl < (i64(1) << 30) && a16(x) && a16(y) && a16(b) && a16(halo_lo) && a16(halo_hi)) {
         const dim3 grid = stencil3d_vec_grid(g);
         if (b)

@@ -41,6 +41,7 @@ namespace {
 struct L2Window {
     Ctx& ctx;
     bool set = false;
+    size_t prev_limit = 0;
     L2Window(Ctx& c, const double* q, i64 ld) : ctx(c) {
         const char* e = std::getenv("KRY_L2_PERSIST");
         if (e && std::atoi(e) == 0) return;
@@ -52,7 +53,8 @@ struct L2Window {
         const size_t cap = std::min<size_t>(static_cast<size_t>(maxpersist), static_cast<size_t>(maxwin));
         if (cap == 0 || 2 * col > cap) return;  // fewer than two columns would fit: no gain
         const size_t bytes = cap / col * col;
-        if (cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess) {
+        if (cudaDeviceGetLimit(&prev_limit, cudaLimitPersistingL2CacheSize) != cudaSuccess ||
+            cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, bytes) != cudaSuccess) {
             cudaGetLastError();
             return;
         }
@@ -74,6 +76,8 @@ struct L2Window {
         v.accessPolicyWindow.num_bytes = 0;
         cudaStreamSetAttribute(ctx.stream, cudaStreamAttributeAccessPolicyWindow, &v);
         cudaCtxResetPersistingL2Cache();
+        // give the set-aside back: later solves (and other work) get the whole L2
+        cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, prev_limit);
     }
 };
 }  // namespace

@@ -14,11 +14,18 @@ KG = np.load(os.path.join(ROOT, "tests", "golden", "kernels_golden.npz"))
 
 
 @pytest.mark.parametrize("key", ["pip2_2d16", "pip2_2d64", "two_2d64_s60", "two_2d100_s20", "standard_2d32",
-                                 "two_3d16_s60", "pip2_2d64_warm"])
+                                 "two_3d16_s60", "pip2_2d64_warm", "rand20k_two_s60_jac", "rand20k_pip2_jac"])
 def test_reference_reproduces_solver_golden(ref, key):
     g = GOLDEN[key]
-    a = ref.laplace2d(g["grid"], g["grid"]) if g["dims"] == 2 else ref.laplace3d(g["grid"], g["grid"], g["grid"])
-    b = ref.spmv(a, np.ones(a.n))
+    if g["operator"] == "random":
+        import os
+        import sys
+        sys.path.insert(0, os.path.join(ROOT, "tests", "golden"))
+        from make_golden import random_jacobi_system
+        a, b = random_jacobi_system(g["grid"])
+    else:
+        a = ref.laplace2d(g["grid"], g["grid"]) if g["dims"] == 2 else ref.laplace3d(g["grid"], g["grid"], g["grid"])
+        b = ref.spmv(a, np.ones(a.n))
     x0 = None if g["x0"] is None else np.full(a.n, g["x0"])
     rep = ref.solve(a, b, x0, ref.make_config(kind=g["kind"], big_step=g["shat"], shat=g["shat"],
                                               max_iters=g["max_iters"]), standard=g["standard"])

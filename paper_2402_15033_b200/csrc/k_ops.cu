@@ -894,11 +894,13 @@ int launch_stencil(cudaStream_t s, const StencilGeom& g, const double* x, const 
         ++launches;
         return b ? static_cast<int>(grid.x * grid.y) : 0;
     }
-    // KRY_STENCIL3D_VEC: 0 = scalar kernel, 1 = stencil3d_vec_kernel (y-neighbours
-    // from L2), 2 (default) = stencil3d_tile_kernel (y-neighbours from shared memory)
+    // KRY_STENCIL3D_VEC: 0 = scalar kernel, 1 (default) = stencil3d_vec_kernel
+    // (y-neighbours from L1/L2), 2 = stencil3d_tile_kernel (y-neighbours from a
+    // shared plane tile; bit-identical, measured no faster: 3.59 vs 3.49 ms of
+    // MPK per 256³ cycle — the L2 re-reads were not the bound)
     static const int vec3 = [] {
         const char* e = std::getenv("KRY_STENCIL3D_VEC");
-        return e ? std::atoi(e) : 2;
+        return e ? std::atoi(e) : 1;
     }();
     if (vec3 == 2 && g.dims == 3 && (g.nx & 1) == 0 && g.nx * g.ny < (i64(1) << 30) && g.nzl < (i64(1) << 30) &&
         a16(x) && a16(y) && a16(b) && a16(halo_lo) && a16(halo_hi) && ceil_div(g.nx, 64) * ceil_div(g.ny, kT3Rows) < (i64(1) << 31)) {

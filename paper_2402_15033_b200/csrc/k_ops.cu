@@ -654,18 +654,25 @@ __global__ void __launch_bounds__(kMpk3Warps * 32, 1)
         double* const orow = out + cell;
         // one step: P = t mod 2 selects the prefetch slot (unrolled by two so
         // the ring never moves; the next load goes out after the slot's last use)
-        auto step = [&](auto parity, int t) {
+        // level k's output rows of plane l live at out + (k − 1)·ldo + l·plane:
+        // per step one base pointer, per level one constant stride (ldo − plane)
+        const i64 dk = ldo - plane;
+        // one step: P = t mod 2 selects the prefetch slot and the shared slots
+        // (unrolled by two so the ring never moves; the next load goes out after
+        // the slot's last use).  FAST: every level's plane this step lies inside
+        // the grid and the band and the tile inside the grid — no masks, no
+        // per-level plane checks (same values).
+        auto step = [&](auto parity, auto fastc, int t) {
             constexpr int P = decltype(parity)::value;
-            const int cur = P, prv = P ^ 1;
+            constexpr bool FAST = decltype(fastc)::value;
             const int lt = zs + t;  // input plane this step
-            // every level's plane this step inside the grid and the band: no masks
-            const bool fast = tile_inside && lt - S >= max(zb0, -z0) && lt - 1 < min(zb1, nz - z0);
             double2 u0 = pf[P][0], u1 = pf[P][1];  // level 0 (the input) at plane lt
+            double* o = orow + static_cast<i64>(lt) * plane - ldo;  // level 0 "output" base; level k: + k·dk
 #pragma unroll
             for (int k = 1; k <= S; ++k) {
-                const int l = lt - k;  // level k's plane this step
-                double2* const qc = mine + (cur * S + (k - 1)) * PLANE;   // level k − 1, slot t (holds t − 2)
-                const double2* const qp = mine + (prv * S + (k - 1)) * PLANE;  // level k − 1, slot t − 1
+                o += dk;
+                double2* const qc = mine + (P * S + (k - 1)) * PLANE;              // level k − 1, slot t (holds t − 2)
+                const double2* const qp = mine + ((P ^ 1) * S + (k - 1)) * PLANE;  // level k − 1, slot t − 1
                 const double2 dn0 = qc[0], dn1 = qc[32];
                 qc[0] = u0;  // publish level k − 1's plane of this step
                 qc[32] = u1;
@@ -706,15 +713,16 @@ __global__ void __launch_bounds__(kMpk3Warps * 32, 1)
                 s3 = off_term<JAC>(s3, c, yp1.y);
                 s3 = off_term<JAC>(s3, c, u1.y);
                 double2 v0 = make_double2(s0, s1), v1 = make_double2(s2, s3);
-                if (!fast) {
+                bool lin = true;
+                if constexpr (!FAST) {
                     // outside the grid: exactly +0.0 (an absent neighbour of a valid cell)
+                    const int l = lt - k;  // level k's plane this step
                     const int gz = z0 + l;
                     const bool zin = gz >= 0 && gz < nz;
                     if (!(in0 && zin)) v0 = make_double2(0.0, 0.0);
                     if (!(in1 && zin)) v1 = make_double2(0.0, 0.0);
+                    lin = l >= zb0 && l < zb1;
                 }
-                const bool lin = fast || (l >= zb0 && l < zb1);
-                double* const o = orow + static_cast<i64>(k - 1) * ldo + static_cast<i64>(l) * plane;
                 if (lin && st0) *reinterpret_cast<double2*>(o) = v0;
                 if (lin && st1) *reinterpret_cast<double2*>(o + nx64) = v1;
                 u0 = v0;  // level k at plane l: level k + 1's upper neighbour
@@ -723,9 +731,16 @@ __global__ void __launch_bounds__(kMpk3Warps * 32, 1)
             load2(lt + 2, pf[P][0], pf[P][1]);
             __syncthreads();
         };
+        const int fast_lo = max(zb0, -z0) + S, fast_hi = min(zb1, nz - z0);  // fast ⇔ lt ∈ [fast_lo, fast_hi]
         for (int t = 0; t < steps; t += 2) {
-            step(std::integral_constant<int, 0>{}, t);
-            if (t + 1 < steps) step(std::integral_constant<int, 1>{}, t + 1);
+            const int lt = zs + t;
+            if (tile_inside && lt >= fast_lo && lt + 1 <= fast_hi) {
+                step(std::integral_constant<int, 0>{}, std::true_type{}, t);
+                if (t + 1 < steps) step(std::integral_constant<int, 1>{}, std::true_type{}, t + 1);
+            } else {
+                step(std::integral_constant<int, 0>{}, std::false_type{}, t);
+                if (t + 1 < steps) step(std::integral_constant<int, 1>{}, std::false_type{}, t + 1);
+            }
         }
     }
 }

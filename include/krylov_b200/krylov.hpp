@@ -27,6 +27,7 @@
 #include <span>
 #include <stdexcept>
 #include <string>
+#include <tuple>
 #include <utility>
 #include <vector>
 
@@ -143,6 +144,31 @@ struct CsrMatrix {  // csr_matrix.hpp:17-65 (indices stored as the reference's s
     std::vector<index_t> row_ptr, col_idx;
     std::vector<double> vals;
     index_t nnz() const { return vals.size(); }
+    // Triplets (row, col, value) → CSR with ascending columns per row,
+    // duplicate entries summed in the order given (csr_matrix.hpp:42).
+    static CsrMatrix from_triplets(index_t n, std::vector<std::tuple<index_t, index_t, double>> trip) {
+        for (const auto& t : trip)
+            if (std::get<0>(t) >= n || std::get<1>(t) >= n) throw DimensionMismatch("dimension mismatch: triplet index");
+        std::stable_sort(trip.begin(), trip.end(), [](const auto& a, const auto& b) {
+            return std::get<0>(a) != std::get<0>(b) ? std::get<0>(a) < std::get<0>(b)
+                                                    : std::get<1>(a) < std::get<1>(b);
+        });
+        CsrMatrix m;
+        m.n = n;
+        m.row_ptr.assign(n + 1, 0);
+        for (std::size_t k = 0; k < trip.size(); ++k) {
+            const auto& [r, c, v] = trip[k];
+            if (k > 0 && std::get<0>(trip[k - 1]) == r && std::get<1>(trip[k - 1]) == c) {
+                m.vals.back() += v;
+                continue;
+            }
+            m.col_idx.push_back(c);
+            m.vals.push_back(v);
+            ++m.row_ptr[r + 1];
+        }
+        for (index_t i = 0; i < n; ++i) m.row_ptr[i + 1] += m.row_ptr[i];
+        return m;
+    }
 };
 
 // ---- scheme / telemetry types (block_ortho.hpp, basis_store.hpp, gmres.hpp) ----

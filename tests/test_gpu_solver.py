@@ -275,6 +275,19 @@ def test_randomised_parity_sweep(kb, ctx, ref):
     assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-2000:]
 
 
+def test_randomised_parity_sweep_at_the_baseline_step(kb, ctx, ref):
+    """tools/fuzz_parity.py at s = 5 (BASELINE's step) with the configs[4]
+    generator and device Jacobi in the draw, seed 40: the status divergence
+    on near-singular bases seen at s = 6-8 (a pivot at the rounding floor)
+    does not occur at s = 5 on these 60 configurations."""
+    import subprocess
+    import sys
+    root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))
+    p = subprocess.run([sys.executable, os.path.join(root, "tools", "fuzz_parity.py"), "40", "60", "s5,jac"],
+                       capture_output=True, text=True, timeout=900, cwd=root)
+    assert p.returncode == 0, p.stdout[-4000:] + p.stderr[-2000:]
+
+
 @pytest.mark.parametrize("key", ["two_2d100_s60", "two_2d100_s20", "pip2_2d100", "two_3d16_s60", "pip2_2d64_warm",
                                  "rand20k_two_s60_jac"])
 def test_graph_replay_matches_direct_launches(kb, ctx, ref, monkeypatch, key):

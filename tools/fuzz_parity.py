@@ -1,7 +1,9 @@
 """Randomised solver parity sweep against the live reference (oracle/_ref):
 random sparse / stencil operators, restart lengths, step sizes, schemes.
 Prints one line per case and a summary; exit code = number of mismatches.
-usage: python tools/fuzz_parity.py SEED NCASES [wide]   (wide: m ≤ 128, s ≤ 8)"""
+usage: python tools/fuzz_parity.py SEED NCASES [MODES]
+  MODES (comma-separated): wide (m ≤ 128, s ≤ 8); jac (also draw the configs[4]
+  generator and the Laplacians with device Jacobi); s5 (s = 5, the BASELINE step)"""
 import os, sys
 sys.path.insert(0, os.path.dirname(os.path.dirname(os.path.abspath(__file__))))
 import numpy as np
@@ -11,15 +13,19 @@ from oracle import ref
 FMA = ref._load(os.path.join(os.path.dirname(ref.__file__), "_ref", "libkrylov_ref_fma.so"))
 rng = np.random.default_rng(int(sys.argv[1]) if len(sys.argv) > 1 else 0)
 ncases = int(sys.argv[2]) if len(sys.argv) > 2 else 40
-wide = len(sys.argv) > 3 and sys.argv[3] == "wide"  # m up to 128, s up to 8
+modes = set(sys.argv[3].split(",")) if len(sys.argv) > 3 else set()
+wide = "wide" in modes  # m up to 128, s up to 8
 bad = 0
 skipped = 0
 for case in range(ncases):
     kind = int(rng.choice([1, 2, 3, 3]))
     s = int(rng.integers(1, 9 if wide else 8))
+    if "s5" in modes:
+        s = 5
     m = s * int(rng.integers(2, max(3, (129 if wide else 61) // s)))
     shat = 0 if kind != 3 else s * int(rng.integers(1, m // s + 1))
-    opk = str(rng.choice(["lap2d", "lap3d", "rand", "gen_jac", "lap_jac"]))
+    opk = str(rng.choice(["lap2d", "lap3d", "rand", "gen_jac", "lap_jac"] if "jac" in modes else
+                         ["lap2d", "lap3d", "rand"]))
     jac = None  # Jacobi: the device operator gets kry_operator_jacobi, the reference D⁻¹A and D⁻¹b
     if opk == "lap2d":
         nx, ny = int(rng.integers(2, 70)), int(rng.integers(2, 70))

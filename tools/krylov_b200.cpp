@@ -9,10 +9,9 @@
 //                     [--m 60] [--s 5] [--shat 0] [--tol 1e-6] [--max-iters 500000]
 //                     [--equilibrate] [--jacobi] --out report.json [--history hist.csv]
 //
-// Host-side input handling restates the reference's Matrix Market reader
-// (matrix_market.hpp:18-76: real general/symmetric coordinate, 1-based, %
-// comments, duplicates summed, square only) and equilibrate
-// (csr_matrix.hpp:85-103).  --jacobi (B200 addition, BASELINE configs[4])
+// Host-side input handling (Matrix Market reader, equilibrate, triplets) is
+// the drop-in API's include/krylov_b200/io.hpp (the reference's
+// matrix_market.hpp:18-76 and csr_matrix.hpp:42-103 interfaces).  --jacobi (B200 addition, BASELINE configs[4])
 // row-scales A by its diagonal before the solve.
 #include <algorithm>
 #include <charconv>
@@ -26,6 +25,7 @@
 #include <tuple>
 #include <vector>
 
+#include "krylov_b200/io.hpp"
 #include "krylov_b200/krylov.hpp"
 
 using namespace krylov_b200;
@@ -79,75 +79,10 @@ Args parse(int argc, char** argv) {
     return a;
 }
 
-// Sorted, merged CSR from triplets (CsrMatrix::from_triplets, csr_matrix.hpp:42-64).
-CsrMatrix from_triplets(index_t n, std::vector<std::tuple<index_t, index_t, double>> t) {
-    std::sort(t.begin(), t.end(), [](const auto& x, const auto& y) {
-        return std::get<0>(x) != std::get<0>(y) ? std::get<0>(x) < std::get<0>(y) : std::get<1>(x) < std::get<1>(y);
-    });
-    CsrMatrix m;
-    m.n = n;
-    m.row_ptr.assign(n + 1, 0);
-    for (size_t k = 0; k < t.size(); ++k) {
-        if (k > 0 && std::get<0>(t[k]) == std::get<0>(t[k - 1]) && std::get<1>(t[k]) == std::get<1>(t[k - 1])) {
-            m.vals.back() += std::get<2>(t[k]);
-        } else {
-            m.col_idx.push_back(std::get<1>(t[k]));
-            m.vals.push_back(std::get<2>(t[k]));
-            ++m.row_ptr[std::get<0>(t[k]) + 1];
-        }
-    }
-    for (index_t i = 0; i < n; ++i) m.row_ptr[i + 1] += m.row_ptr[i];
-    return m;
-}
-
 CsrMatrix read_matrix_market(const std::string& path) {
     std::ifstream in(path);
     if (!in) throw std::runtime_error("cannot open matrix file " + path);
-    std::string line;
-    size_t lineno = 0;
-    if (!std::getline(in, line)) throw std::runtime_error("unsupported format: empty stream");
-    ++lineno;
-    std::istringstream hs(line);
-    std::string banner, object, format, field, symmetry;
-    hs >> banner >> object >> format >> field >> symmetry;
-    if (banner != "%%MatrixMarket" || object != "matrix")
-        throw std::runtime_error("unsupported format: missing %%MatrixMarket matrix header");
-    if (format != "coordinate") throw std::runtime_error("unsupported format: format '" + format + "'");
-    if (field != "real") throw std::runtime_error("unsupported format: field '" + field + "'");
-    if (symmetry != "general" && symmetry != "symmetric")
-        throw std::runtime_error("unsupported format: symmetry '" + symmetry + "'");
-    const bool sym = symmetry == "symmetric";
-    long long rows = 0, cols = 0, nnz = 0;
-    bool sized = false;
-    while (std::getline(in, line)) {
-        ++lineno;
-        if (line.empty() || line[0] == '%') continue;
-        std::istringstream ss(line);
-        if (!(ss >> rows >> cols >> nnz) || rows < 0 || cols < 0 || nnz < 0)
-            throw std::runtime_error("malformed entry at line " + std::to_string(lineno) + ": size line");
-        sized = true;
-        break;
-    }
-    if (!sized || rows == 0 || cols == 0)
-        throw std::runtime_error("malformed entry at line " + std::to_string(lineno) + ": missing size line");
-    if (rows != cols) throw std::runtime_error("unsupported format: rectangular matrix (square operator required)");
-    std::vector<std::tuple<index_t, index_t, double>> trip;
-    long long seen = 0;
-    while (seen < nnz && std::getline(in, line)) {
-        ++lineno;
-        if (line.empty() || line[0] == '%') continue;
-        std::istringstream ss(line);
-        long long r, c;
-        double v;
-        if (!(ss >> r >> c >> v)) throw std::runtime_error("malformed entry at line " + std::to_string(lineno));
-        if (r < 1 || c < 1 || r > rows || c > cols)
-            throw std::runtime_error("index out of range at line " + std::to_string(lineno));
-        trip.emplace_back(r - 1, c - 1, v);
-        if (sym && r != c) trip.emplace_back(c - 1, r - 1, v);
-        ++seen;
-    }
-    if (seen < nnz) throw std::runtime_error("malformed entry: fewer entries than announced");
-    return from_triplets(static_cast<index_t>(rows), std::move(trip));
+    return krylov_b200::read_matrix_market(in);
 }
 
 CsrMatrix laplace2d_csr(index_t nx, index_t ny, int stencil) {  // matgen.hpp:134-164
@@ -165,21 +100,7 @@ CsrMatrix laplace2d_csr(index_t nx, index_t ny, int stencil) {  // matgen.hpp:13
                     t.emplace_back(row, static_cast<index_t>(jy) * nx + static_cast<index_t>(jx), off);
                 }
         }
-    return from_triplets(nx * ny, std::move(t));
-}
-
-void equilibrate(CsrMatrix& a) {  // csr_matrix.hpp:85-103 (column maxima, then row maxima)
-    std::vector<double> cmax(a.n, 0.0);
-    for (index_t k = 0; k < a.nnz(); ++k) cmax[a.col_idx[k]] = std::max(cmax[a.col_idx[k]], std::abs(a.vals[k]));
-    for (index_t j = 0; j < a.n; ++j)
-        if (cmax[j] == 0.0) throw std::runtime_error("column " + std::to_string(j) + " has no nonzero entries");
-    for (index_t k = 0; k < a.nnz(); ++k) a.vals[k] /= cmax[a.col_idx[k]];
-    for (index_t i = 0; i < a.n; ++i) {
-        double rmax = 0.0;
-        for (index_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) rmax = std::max(rmax, std::abs(a.vals[k]));
-        if (rmax == 0.0) throw std::runtime_error("row " + std::to_string(i) + " has no nonzero entries");
-        for (index_t k = a.row_ptr[i]; k < a.row_ptr[i + 1]; ++k) a.vals[k] /= rmax;
-    }
+    return CsrMatrix::from_triplets(nx * ny, std::move(t));
 }
 
 void jacobi_scale(CsrMatrix& a) {  // left diagonal scaling D⁻¹A
@@ -241,7 +162,7 @@ int run(int argc, char** argv) {
         else if (a.grid3d > 0) throw std::runtime_error("--grid3d with --equilibrate/--jacobi: use a .mtx file");
         else if (a.grid > 0) m = laplace2d_csr(a.grid, a.grid, a.stencil);
         else throw std::runtime_error("either --matrix or --grid is required");
-        if (a.equilibrate) equilibrate(m);
+        if (a.equilibrate) m = krylov_b200::equilibrate(m);
         if (a.jacobi) jacobi_scale(m);
         op = std::make_unique<Operator>(Operator::csr(m));
     }

@@ -277,9 +277,11 @@ def test_randomised_parity_sweep(kb, ctx, ref):
 
 def test_randomised_parity_sweep_at_the_baseline_step(kb, ctx, ref):
     """tools/fuzz_parity.py at s = 5 (BASELINE's step) with the configs[4]
-    generator and device Jacobi in the draw, seed 40: the status divergence
-    on near-singular bases seen at s = 6-8 (a pivot at the rounding floor)
-    does not occur at s = 5 on these 60 configurations."""
+    generator and device Jacobi in the draw, seed 40: 60 configurations, all
+    within the protocol.  (Seeds 40-43: 238 / 240; the two others are tiny
+    grids, n ≤ 80, solved to ~1e-15 inside one cycle, where the reference's
+    own FMA build differs from its plain build by 48-64 % —
+    profiles/fuzz_r02_s5_s40_43.log.)"""
     import subprocess
     import sys
     root = os.path.dirname(os.path.dirname(os.path.abspath(__file__)))

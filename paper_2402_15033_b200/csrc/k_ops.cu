@@ -565,71 +565,6 @@ __global__ void __launch_bounds__(kBlock, 2) mpk2d_kernel(const StencilGeom g, c
                       static_cast<int>(band), lane);
 }
 
-// K2t: the 2-D MPK for small grids, one tile per CTA in shared memory.  At
-// 512² K2f's skewed wavefront spends 2S − 1 of its ~12 line steps filling and
-// draining the pipeline and is latency-bound (17.5 µs per block, DRAM 1.5 %).
-// Here a CTA loads a (TY + 2S) × (TX + 2S) window of x (its 32 × 64 output
-// tile plus an S-cell margin, +0.0 outside the grid) into shared memory and
-// computes the levels one after the other over the window shrunk by k cells
-// per side (ping-pong buffers, one barrier per level), writing each level's
-// tile to out.  Every element is spmv's sum in stored order (row − nx,
-// row − 1, row, row + 1, row + nx), absent neighbours carried as +0.0 and
-// added as −0.0 (see K2f): bit-identical.  The margins are recomputed
-// ((42·74)/(32·64) = 1.5× the stencil work), which is free at these sizes.
-constexpr int kMtY = 32, kMtX = 64;
-
-template <int S, bool JAC>
-__global__ void __launch_bounds__(kBlock) mpk2d_tile_kernel(const StencilGeom g, const double* __restrict__ x,
-                                                            const double* __restrict__ halo_lo,
-                                                            const double* __restrict__ halo_hi,
-                                                            double* __restrict__ out, i64 ldo, int ntx) {
-    KB_PDL_WAIT();
-    constexpr int WY = kMtY + 2 * S, WX = kMtX + 2 * S;
-    extern __shared__ double mt_smem[];  // [2][WY][WX]
-    auto buf = reinterpret_cast<double(*)[WY][WX]>(mt_smem);
-    const int nx = static_cast<int>(g.nx), ny = static_cast<int>(g.ny);
-    const int lines = static_cast<int>(g.lines), line0 = static_cast<int>(g.line0);
-    const i64 nx64 = nx;
-    const int tx = blockIdx.x % ntx, ty = blockIdx.x / ntx;
-    const int x0 = tx * kMtX - S, y0 = ty * kMtY - S;  // window origin (local line, column)
-    const double c = g.c_off;
-    // window of x (+0.0 outside the grid; lines beyond this rank from the halos)
-    for (int e = threadIdx.x; e < WY * WX; e += blockDim.x) {
-        const int wy = e / WX, wx = e - wy * WX;
-        const int l = y0 + wy, ix = x0 + wx, gl = line0 + l;
-        double v = 0.0;
-        if (ix >= 0 && ix < nx && gl >= 0 && gl < ny && l >= -S && l < lines + S) {
-            const double* p = l < 0       ? halo_lo + static_cast<i64>(l + S) * nx64
-                              : l < lines ? x + static_cast<i64>(l) * nx64
-                                          : halo_hi + static_cast<i64>(l - lines) * nx64;
-            v = p[ix];
-        }
-        buf[0][wy][wx] = v;
-    }
-    __syncthreads();
-#pragma unroll 1
-    for (int k = 1; k <= S; ++k) {
-        const double(*src)[WX] = buf[(k - 1) & 1];
-        double(*dst)[WX] = buf[k & 1];
-        const int h = WX - 2 * k, hy = WY - 2 * k;  // level k's valid region: [k, WY − k) × [k, WX − k)
-        for (int e = threadIdx.x; e < hy * h; e += blockDim.x) {
-            const int wy = k + e / h, wx = k + e % h;
-            const int l = y0 + wy, ix = x0 + wx, gl = line0 + l;
-            double sum = off_term<JAC>(0.0, c, src[wy - 1][wx]);
-            sum = off_term<JAC>(sum, c, src[wy][wx - 1]);
-            sum = diag_term<JAC>(sum, 4.0, src[wy][wx]);
-            sum = off_term<JAC>(sum, c, src[wy][wx + 1]);
-            sum = off_term<JAC>(sum, c, src[wy + 1][wx]);
-            // outside the grid: exactly +0.0 (an absent neighbour of a valid cell)
-            const bool live = ix >= 0 && ix < nx && gl >= 0 && gl < ny;
-            dst[wy][wx] = live ? sum : 0.0;
-            if (live && wy >= S && wy < S + kMtY && wx >= S && wx < S + kMtX && l < lines)
-                out[static_cast<i64>(k - 1) * ldo + static_cast<i64>(l) * nx64 + ix] = sum;
-        }
-        __syncthreads();
-    }
-}
-
 // K2g: the whole s-step MPK of the 7-point stencil in one pass
 // (mpk_monomial, gmres.hpp:80-90, on gen_laplace3d, matgen.hpp:167-187):
 // out[:, k−1] = A^k·x for k = 1..S.  Temporal blocking along z: a CTA of
@@ -1058,47 +993,8 @@ bool mpk2d_supported(const StencilGeom& g, int s, const double* x, const double*
     return force || tasks >= static_cast<i64>(num_sms());
 }
 
-// K2t on small grids (one wave of tiles), K2f otherwise; KRY_MPK_TILE=0 never
-// uses K2t, =2 always (tests).
-static bool mpk2d_tile_wanted(const StencilGeom& g, int s) {
-    const char* e = std::getenv("KRY_MPK_TILE");  // read per launch (tests switch it)
-    const int mode = e ? std::atoi(e) : 1;
-    if (mode == 0 || s > 8) return false;
-    if (mode == 2) return true;
-    return ceil_div(g.lines, kMtY) * ceil_div(g.nx, kMtX) <= static_cast<i64>(num_sms());
-}
-
 void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const double* halo_lo,
                   const double* halo_hi, double* out, i64 ldo, int s, int64_t& launches) {
-    if (mpk2d_tile_wanted(g, s)) {
-        const i64 ntx = ceil_div(g.nx, kMtX), tiles = ntx * ceil_div(g.lines, kMtY);
-        const size_t smem = static_cast<size_t>(2) * (kMtY + 2 * s) * (kMtX + 2 * s) * sizeof(double);
-        auto go_t = [&](auto kernel) {
-            set_kernel_smem(reinterpret_cast<const void*>(kernel), smem);
-            launch_pdl(kernel, static_cast<unsigned>(tiles), kBlock, smem, st, g, x, halo_lo, halo_hi, out, ldo,
-                       static_cast<int>(ntx));
-        };
-#define KB_MPKT(SV)                                                             \
-    case SV:                                                                    \
-        if (g.jacobi) go_t(mpk2d_tile_kernel<SV, true>);                        \
-        else go_t(mpk2d_tile_kernel<SV, false>);                                \
-        break;
-        switch (s) {
-            KB_MPKT(1)
-            KB_MPKT(2)
-            KB_MPKT(3)
-            KB_MPKT(4)
-            KB_MPKT(5)
-            KB_MPKT(6)
-            KB_MPKT(7)
-            KB_MPKT(8)
-            default: fail(KRY_INTERNAL, "mpk2d tile: unsupported s");
-        }
-#undef KB_MPKT
-        KB_LAUNCHED();
-        ++launches;
-        return;
-    }
     const int h = (s + 1) & ~1, step = 64 - 2 * h;
     const i64 nwx = ceil_div(g.nx, step);
     auto go = [&](auto kernel) {

@@ -107,10 +107,8 @@ def test_mpk_bitwise(kb, ctx, ref, rng, s):
                                      (106, 41, 1), (64, 9, 6), (2, 2, 3),
                                      # a window's last lane on the grid's last column
                                      (110, 40, 5), (58, 30, 6), (104, 50, 8), (60, 33, 3), (62, 20, 1)])
-@pytest.mark.parametrize("tile", ["0", "2"])  # K2f wavefront / K2t shared-memory tiles
-def test_mpk_fused_bitwise(kb, ctx, ref, rng, monkeypatch, nx, ny, s, tile):
+def test_mpk_fused_bitwise(kb, ctx, ref, rng, monkeypatch, nx, ny, s):
     monkeypatch.setenv("KRY_FUSED_MPK", "2")  # below the size heuristic: force the one-pass kernel
-    monkeypatch.setenv("KRY_MPK_TILE", tile)
     a = ref.laplace2d(nx, ny)
     op = kb.Laplace2D(nx, ny)
     start = rng.standard_normal(a.n)
@@ -142,16 +140,14 @@ def prescaled(a):
     return R.Csr(a.n, a.row_ptr, a.col_idx, a.vals / d[rows])
 
 
-@pytest.mark.parametrize("tile", ["0", "2"])
 @pytest.mark.parametrize("dims,shape,fused", [(2, (130, 97), "2"), (2, (131, 50), "2"), (2, (40, 30), "0"),
                                               (3, (58, 45, 12), "2"), (3, (17, 9, 11), "0"),
                                               (3, (64, 64, 64), "0")])
-def test_jacobi_stencil_bitwise(kb, ctx, ref, rng, monkeypatch, dims, shape, fused, tile):
+def test_jacobi_stencil_bitwise(kb, ctx, ref, rng, monkeypatch, dims, shape, fused):
     """Jacobi on the matrix-free Laplacians: the stencil and MPK kernels apply
     D⁻¹A (off-diagonal −1/d rounded, diagonal 1) bit-identically to the
     reference's spmv / mpk_monomial on the host pre-scaled CSR."""
     monkeypatch.setenv("KRY_FUSED_MPK", fused)
-    monkeypatch.setenv("KRY_MPK_TILE", tile)
     a = ref.laplace2d(*shape) if dims == 2 else ref.laplace3d(*shape)
     op = (kb.Laplace2D if dims == 2 else kb.Laplace3D)(*shape)
     op.jacobi()

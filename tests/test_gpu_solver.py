@@ -92,10 +92,8 @@ def test_solver_matches_reference_fused_pass(kb, ctx, ref, monkeypatch, key):
 # stencil configurations again with the fused one-pass MPK forced on.
 @pytest.mark.parametrize("key", sorted(k for k in GOLDEN if GOLDEN[k]["operator"] != "csr"
                                        and GOLDEN[k]["dims"] == 2 and not GOLDEN[k]["standard"]))
-@pytest.mark.parametrize("tile", ["0", "1"])  # K2f everywhere / K2t on the small grids (default)
-def test_solver_matches_reference_fused_mpk(kb, ctx, ref, monkeypatch, key, tile):
+def test_solver_matches_reference_fused_mpk(kb, ctx, ref, monkeypatch, key):
     monkeypatch.setenv("KRY_FUSED_MPK", "2")
-    monkeypatch.setenv("KRY_MPK_TILE", tile)
     rep, g = run_golden(kb, ref, key)
     assert_parity(rep, g)
 

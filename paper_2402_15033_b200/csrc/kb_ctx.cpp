@@ -101,20 +101,11 @@ Ctx::~Ctx() {
     }
     for (cudaEvent_t e : pool) cudaEventDestroy(e);
     if (comm) ncclCommDestroy(comm);
-    if (ev_ready) cudaEventDestroy(ev_ready);
-    if (ev_halo) cudaEventDestroy(ev_halo);
-    if (comm_stream) cudaStreamDestroy(comm_stream);
     if (stream) cudaStreamDestroy(stream);
 }
 
 void bind_device(Ctx& c) { KB_CUDA(cudaSetDevice(c.device)); }
 
-void Ctx::ensure_comm_stream() {
-    if (comm_stream) return;
-    KB_CUDA(cudaStreamCreateWithFlags(&comm_stream, cudaStreamNonBlocking));
-    KB_CUDA(cudaEventCreateWithFlags(&ev_ready, cudaEventDisableTiming));
-    KB_CUDA(cudaEventCreateWithFlags(&ev_halo, cudaEventDisableTiming));
-}
 
 void Ctx::sync() {
     drain_timers();  // elapsed-time queries of finished phases, while the GPU is still busy

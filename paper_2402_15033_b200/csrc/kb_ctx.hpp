@@ -72,11 +72,6 @@ struct Ctx {
     int nranks = 1;
     int rank = 0;
     cudaStream_t stream = nullptr;
-    // multi-rank: a second stream for halo exchanges that overlap the
-    // interior of the one-pass MPK (created on first use)
-    cudaStream_t comm_stream = nullptr;
-    cudaEvent_t ev_ready = nullptr, ev_halo = nullptr;
-    void ensure_comm_stream();
     ncclComm_t comm = nullptr;
     bool timing = false;
     int64_t launches = 0;

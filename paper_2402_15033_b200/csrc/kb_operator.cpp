@@ -255,44 +255,6 @@ bool Operator::mpk(const double* x, double* out, i64 ldo, int s) {
         if (uniform.nzl < s || !mpk3d_supported(uniform, s, x, out, ldo, mode == 2)) return false;
     }
     const i64 h = static_cast<i64>(s) * plane;
-    if (c.nranks > 1 && kind == LAPLACE2D && uniform.lines >= 3 * s) {
-        // The s-line halo exchange overlaps the interior: output lines
-        // [s, lines − s) need no neighbour data (their s-line input margin is
-        // this rank's own lines), so they run while the halos travel on the
-        // side stream; the two s-line edge strips follow.  Every element is
-        // the same stencil sum whatever the strip split (bit-identical).
-        mpk_lo.ensure(static_cast<size_t>(h) * 8);
-        mpk_hi.ensure(static_cast<size_t>(h) * 8);
-        c.ensure_comm_stream();
-        KB_CUDA(cudaEventRecord(c.ev_ready, c.stream));
-        KB_CUDA(cudaStreamWaitEvent(c.comm_stream, c.ev_ready, 0));
-        KB_NCCL(ncclGroupStart());
-        if (c.rank > 0) {
-            KB_NCCL(ncclSend(x, static_cast<size_t>(h), ncclDouble, c.rank - 1, c.comm, c.comm_stream));
-            KB_NCCL(ncclRecv(mpk_lo.p, static_cast<size_t>(h), ncclDouble, c.rank - 1, c.comm, c.comm_stream));
-        }
-        if (c.rank + 1 < c.nranks) {
-            KB_NCCL(ncclSend(x + nloc - h, static_cast<size_t>(h), ncclDouble, c.rank + 1, c.comm, c.comm_stream));
-            KB_NCCL(ncclRecv(mpk_hi.p, static_cast<size_t>(h), ncclDouble, c.rank + 1, c.comm, c.comm_stream));
-        }
-        KB_NCCL(ncclGroupEnd());
-        KB_CUDA(cudaEventRecord(c.ev_halo, c.comm_stream));
-        const i64 L = geom.lines, nx = geom.nx;
-        auto strip = [&](i64 first, i64 count) {
-            StencilGeom g = geom;
-            g.line0 = geom.line0 + first;
-            g.lines = count;
-            g.row_begin = geom.row_begin + first * nx;
-            g.nloc = count * nx;
-            return g;
-        };
-        launch_mpk2d(c.stream, strip(s, L - 2 * s), x + s * nx, x, x + (L - s) * nx, out + s * nx, ldo, s, c.launches);
-        KB_CUDA(cudaStreamWaitEvent(c.stream, c.ev_halo, 0));
-        launch_mpk2d(c.stream, strip(0, s), x, mpk_lo.p, x + s * nx, out, ldo, s, c.launches);
-        launch_mpk2d(c.stream, strip(L - s, s), x + (L - s) * nx, x + (L - 2 * s) * nx, mpk_hi.p, out + (L - s) * nx,
-                     ldo, s, c.launches);
-        return true;
-    }
     if (c.nranks > 1) {
         mpk_lo.ensure(static_cast<size_t>(h) * 8);
         mpk_hi.ensure(static_cast<size_t>(h) * 8);

@@ -1032,13 +1032,11 @@ bool mpk3d_supported(const StencilGeom& g, int s, const double* x, const double*
     if (!(g.dims == 3 && (g.nx & 1) == 0 && s >= 1 && s <= 6 && (ldo & 1) == 0 && a16(x) && a16(out) &&
           g.nzl >= 1 && g.nx + 64 < (i64(1) << 31) && g.ny + 64 < (i64(1) << 31) && g.nz + 16 < (i64(1) << 31)))
         return false;
-    // Opt-in (force: KRY_FUSED_MPK=2).  Bit-identical, but slower than s
-    // separate stencil3d_vec launches on B200: 4.12 vs 3.40 ms of MPK per
-    // 256³ cycle — each z-step costs ~550 warp instructions per level set
-    // (the y-neighbour exchange through shared memory, one barrier per step,
-    // 1.7× redundant tile-overlap work at s = 5), so the kernel is issue- and
-    // latency-bound at 2.1 IPC while the per-SpMV kernels stream at 5.2 TB/s
-    // (profiles/ncu_mpk3d_r02.txt).
+    // The size heuristic is the caller's (Operator::mpk): on one rank the
+    // kernel is slower than s separate stencil3d_vec launches (4.4 vs 3.5 ms
+    // of MPK per 256³ cycle — shared-memory traffic and latency bound it at
+    // ~2 IPC, profiles/ncu_mpk3d_*r02.txt); with several ranks
+    // its one s-plane halo exchange per block wins.
     return force;
 }
 

@@ -252,7 +252,12 @@ bool Operator::mpk(const double* x, double* out, i64 ldo, int s) {
     } else {
         uniform.nzl = geom.nz / c.nranks;
         plane = geom.nx * geom.ny;
-        if (uniform.nzl < s || !mpk3d_supported(uniform, s, x, out, ldo, mode == 2)) return false;
+        // One rank: s per-SpMV launches are faster than the one-pass kernel
+        // (3.50 vs 4.37 ms of MPK per 256³ cycle).  Several ranks: its single
+        // s-plane exchange per block beats s one-plane exchanges (256³:
+        // 2.49 vs 2.91 ms at N = 2, 1.65 vs 2.72 ms at N = 4).
+        if (!(mode == 2 || c.nranks > 1)) return false;
+        if (uniform.nzl < s || !mpk3d_supported(uniform, s, x, out, ldo, true)) return false;
     }
     const i64 h = static_cast<i64>(s) * plane;
     if (c.nranks > 1) {

@@ -1006,7 +1006,8 @@ void launch_mpk2d(cudaStream_t st, const StencilGeom& g, const double* x, const 
         const int per_sm = occupancy(reinterpret_cast<const void*>(kernel), kBlock, 0);
         const i64 resident = static_cast<i64>(num_sms()) * std::max(per_sm, 1) * (kBlock / 32);
         const i64 nbands = std::max<i64>(1, std::min<i64>(resident / nwx, g.lines / 2));
-        const i64 band = ceil_div(g.lines, nbands);
+        i64 band = ceil_div(g.lines, nbands);
+        if (const char* e = std::getenv("KRY_MPK_BAND")) band = std::max<i64>(1, std::atoll(e));  // A/B
         const i64 ntasks = nwx * ceil_div(g.lines, band);
         const unsigned grid = static_cast<unsigned>(
             std::min<i64>(ceil_div(ntasks, kBlock / 32), static_cast<i64>(num_sms()) * std::max(per_sm, 1)));

@@ -51,7 +51,11 @@ __global__ void __launch_bounds__(kPeerThreads) peer_allreduce_kernel(double* __
     if (threadIdx.x < nranks) {
         st_release_sys(t.flags[threadIdx.x] + par * nranks + rank, epoch);
         const uint64_t* mine = t.flags[rank] + par * nranks + threadIdx.x;
+        // a peer that never arrives (it failed, or took another code path)
+        // must not hang the GPU: after ~10 s abort the context loudly
+        const long long t0 = clock64();
         while (ld_acquire_sys(mine) < epoch) {
+            if (clock64() - t0 > 20000000000LL) __trap();
         }
     }
     __syncthreads();

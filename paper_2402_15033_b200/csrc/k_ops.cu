@@ -264,6 +264,11 @@ __global__ void __launch_bounds__(kBlock, 6) stencil3d_vec_kernel(const StencilG
     const bool has_ym = iy > 0, has_yp = iy + 1 < ny, has_l = ix > 0, has_r = ix + 2 < nx;
     const int lane = threadIdx.x & 31;
     auto ld2 = [](const double* p) { return *reinterpret_cast<const double2*>(p); };
+    // every lane of the warp has all four in-plane neighbours (the lanes at
+    // the warp's ends still read their outer x-neighbour from memory): the
+    // interior planes then take a branch-free path (same terms, same order;
+    // MPK 3.28 -> 3.21 ms per 256³ cycle, profiles/stencil3d_fast_ab_r02.log)
+    const bool warp_inside = __all_sync(0xffffffffu, active && has_ym && has_yp && has_l && has_r);
     double sq = 0.0;
     const int nzl = static_cast<int>(g.nzl), nz = static_cast<int>(g.nz), z0 = static_cast<int>(g.z0);
     for (int zc = blockIdx.y * kPlanesPerThread; zc < nzl; zc += gridDim.y * kPlanesPerThread) {
@@ -284,7 +289,35 @@ __global__ void __launch_bounds__(kBlock, 6) stencil3d_vec_kernel(const StencilG
             if (active && has_up) up = l + 1 < nzl ? ld2(xc + plane) : ld2(halo_hi + off);
             double left = __shfl_up_sync(0xffffffffu, cur.y, 1);
             double right = __shfl_down_sync(0xffffffffu, cur.x, 1);
-            if (active) {
+            if (warp_inside && has_dn && has_up) {
+                if (lane == 0) left = xc[-1];
+                if (lane == 31) right = xc[2];
+                const double2 ym = ld2(xc - nx), yp = ld2(xc + nx);
+                double s0 = off_term<JAC>(0.0, g.c_off, down.x);
+                s0 = off_term<JAC>(s0, g.c_off, ym.x);
+                s0 = off_term<JAC>(s0, g.c_off, left);
+                s0 = diag_term<JAC>(s0, 6.0, cur.x);
+                s0 = off_term<JAC>(s0, g.c_off, cur.y);
+                s0 = off_term<JAC>(s0, g.c_off, yp.x);
+                s0 = off_term<JAC>(s0, g.c_off, up.x);
+                double s1 = off_term<JAC>(0.0, g.c_off, down.y);
+                s1 = off_term<JAC>(s1, g.c_off, ym.y);
+                s1 = off_term<JAC>(s1, g.c_off, cur.x);
+                s1 = diag_term<JAC>(s1, 6.0, cur.y);
+                s1 = off_term<JAC>(s1, g.c_off, right);
+                s1 = off_term<JAC>(s1, g.c_off, yp.y);
+                s1 = off_term<JAC>(s1, g.c_off, up.y);
+                if (RESID) {
+                    const double2 bb = ld2(bc);
+                    bc += plane;
+                    const double r0 = __dsub_rn(bb.x, s0), r1 = __dsub_rn(bb.y, s1);
+                    *reinterpret_cast<double2*>(yc) = make_double2(r0, r1);
+                    sq = fma(r0, r0, sq);
+                    sq = fma(r1, r1, sq);
+                } else {
+                    *reinterpret_cast<double2*>(yc) = make_double2(s0, s1);
+                }
+            } else if (active) {
                 if (lane == 0 && has_l) left = xc[-1];
                 if (lane == 31 && has_r) right = xc[2];
                 const double2 ym = has_ym ? ld2(xc - nx) : make_double2(0.0, 0.0);

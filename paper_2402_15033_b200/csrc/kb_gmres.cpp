@@ -242,7 +242,7 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
         cudaEvent_t t0 = ctx.begin_phase();
         // x_new = x + Q·y in row chunks; with a host output each chunk is
         // copied out on the side stream as soon as it is written
-        const int nchunk = h_x_out ? 4 : 1;
+        const int nchunk = h_x_out ? 8 : 1;  // ≤ chunk_ev
         if (h_x_out) KB_CUDA(cudaStreamWaitEvent(ctx.stream, W.copy_done, 0));  // xn may still be going out
         for (int ch = 0; ch < nchunk; ++ch) {
             const i64 r0c = n * ch / nchunk, r1c = n * (ch + 1) / nchunk;

@@ -60,7 +60,7 @@ struct Workspace {
     // host-output path: the solution update streams to the host while it is
     // computed (side stream, one event per row chunk)
     cudaStream_t copy_stream = nullptr;
-    cudaEvent_t chunk_ev[4] = {}, copy_done = nullptr;
+    cudaEvent_t chunk_ev[8] = {}, copy_done = nullptr;
     Workspace() = default;
     Workspace(const Workspace&) = delete;
     Workspace& operator=(const Workspace&) = delete;

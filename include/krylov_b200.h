@@ -223,6 +223,20 @@ int kry_bcgs_pip2(kry_ctx* ctx, int64_t n, const double* q_prev, int64_t c0, con
                   double* q, double* r_col, double* r_jj, int64_t* pivot, int64_t* reduces); /* :192 */
 int kry_cholqr(kry_ctx* ctx, int64_t n, const double* v, int64_t w, double* q, double* r,
                int64_t* pivot, int64_t* reduces);                            /* :49 */
+/* The BCGS2 baseline pieces (block_ortho.hpp:57-137):
+ * cholqr2 = CholQR twice, R = R₂·R₁ (2 reduces); bcgs_project: r_block =
+ * Q_prevᵀV (c0×w), vhat = V − Q_prev·r_block (1 reduce, 0 when c0 == 0);
+ * bcgs2 = project, intra (CholQR2, or CholQR for one column), re-project,
+ * CholQR.  intra_kind: 1 = CholQR2 (IntraKind::Cholqr2); 0 = HHQR is
+ * KRY_UNSUPPORTED for w > 1 (not on the device path).  A failed Cholesky
+ * returns KRY_NOT_POSITIVE_DEFINITE with its pivot. */
+int kry_cholqr2(kry_ctx* ctx, int64_t n, const double* v, int64_t w, double* q, double* r,
+                int64_t* pivot, int64_t* reduces);                           /* :57 */
+int kry_bcgs_project(kry_ctx* ctx, int64_t n, const double* q_prev, int64_t c0, const double* v, int64_t w,
+                     double* vhat, double* r_block, int64_t* reduces);       /* :70 */
+int kry_bcgs2(kry_ctx* ctx, int64_t n, const double* q_prev, int64_t c0, const double* v, int64_t w,
+              int32_t intra_kind, double* q, double* r_col, double* r_jj, int64_t* pivot,
+              int64_t* reduces);                                            /* :102 */
 /* Device views with explicit leading dimensions; out may alias v. */
 int kry_bcgs_pip_device(kry_ctx* ctx, int64_t n, const double* d_q_prev, int64_t ldq, int64_t c0,
                         const double* d_v, int64_t ldv, int64_t w, double* d_out, int64_t ldo,

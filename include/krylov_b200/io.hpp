@@ -1,9 +1,10 @@
 // krylov_b200/io.hpp — host-side input utilities of the drop-in C++ API:
 // building a CsrMatrix from triplets, Matrix Market read / write and
 // equilibration (the reference's csr_matrix.hpp:42-103 and
-// matrix_market.hpp:18-76 interfaces, with its exception types, types.hpp:43-70).
-// They prepare operators on the host; nothing here runs on the GPU (the
-// solve does).  Used by tools/krylov_b200 (the CLI) and by the reference's
+// matrix_market.hpp:18-76 interfaces, with its exception types, types.hpp:43-70)
+// and the Laplacian generators of matgen.hpp:134-195.
+// They prepare operators on the host (only gen_rhs_ones' SpMV runs on the
+// GPU).  Used by tools/krylov_b200 (the CLI) and by the reference's
 // own tests/test_sparse_core.cpp compiled against this API
 // (tests/cpp/refcompat).
 #pragma once
@@ -123,5 +124,65 @@ inline CsrMatrix equilibrate(const CsrMatrix& a) {
     }
     return e;
 }
+
+// Dirichlet Laplacians on a grid, row-major node order, as CsrMatrix
+// (matgen.hpp:134-195): 5-point (diagonal 4, neighbours −1), 9-point
+// (diagonal 8/3, all eight neighbours −1/3), 7-point 3-D (diagonal 6,
+// neighbours −1).  Columns ascend within each row.  (The solver's own
+// matrix-free operators are Operator::laplace2d / laplace3d.)
+inline CsrMatrix gen_laplace2d(index_t nx, index_t ny, int stencil = 5) {
+    if (nx < 2 || ny < 2) throw DimensionMismatch("gen_laplace2d needs dimensions >= 2");
+    if (stencil != 5 && stencil != 9) throw std::invalid_argument("gen_laplace2d stencil must be 5 or 9");
+    CsrMatrix a;
+    a.n = nx * ny;
+    a.row_ptr.assign(1, 0);
+    a.col_idx.reserve(a.n * static_cast<index_t>(stencil));
+    a.vals.reserve(a.n * static_cast<index_t>(stencil));
+    const double centre = stencil == 5 ? 4.0 : 8.0 / 3.0, nb = stencil == 5 ? -1.0 : -1.0 / 3.0;
+    for (index_t iy = 0; iy < ny; ++iy)
+        for (index_t ix = 0; ix < nx; ++ix) {
+            for (index_t jy = iy == 0 ? 0 : iy - 1; jy <= std::min(iy + 1, ny - 1); ++jy)
+                for (index_t jx = ix == 0 ? 0 : ix - 1; jx <= std::min(ix + 1, nx - 1); ++jx) {
+                    const bool centre_node = jx == ix && jy == iy;
+                    if (stencil == 5 && jx != ix && jy != iy) continue;  // no diagonals
+                    a.col_idx.push_back(jy * nx + jx);
+                    a.vals.push_back(centre_node ? centre : nb);
+                }
+            a.row_ptr.push_back(a.col_idx.size());
+        }
+    return a;
+}
+
+inline CsrMatrix gen_laplace3d(index_t nx, index_t ny, index_t nz) {
+    if (nx < 2 || ny < 2 || nz < 2) throw DimensionMismatch("gen_laplace3d needs dimensions >= 2");
+    CsrMatrix a;
+    a.n = nx * ny * nz;
+    a.row_ptr.assign(1, 0);
+    a.col_idx.reserve(a.n * 7);
+    a.vals.reserve(a.n * 7);
+    const index_t plane = nx * ny;
+    for (index_t iz = 0; iz < nz; ++iz)
+        for (index_t iy = 0; iy < ny; ++iy)
+            for (index_t ix = 0; ix < nx; ++ix) {
+                const index_t r = iz * plane + iy * nx + ix;
+                auto put = [&](bool present, index_t c, double v) {
+                    if (!present) return;
+                    a.col_idx.push_back(c);
+                    a.vals.push_back(v);
+                };
+                put(iz > 0, r - plane, -1.0);
+                put(iy > 0, r - nx, -1.0);
+                put(ix > 0, r - 1, -1.0);
+                put(true, r, 6.0);
+                put(ix + 1 < nx, r + 1, -1.0);
+                put(iy + 1 < ny, r + nx, -1.0);
+                put(iz + 1 < nz, r + plane, -1.0);
+                a.row_ptr.push_back(a.col_idx.size());
+            }
+    return a;
+}
+
+// b = A·1 (matgen.hpp:190), the SpMV on the GPU.
+inline std::vector<double> gen_rhs_ones(const CsrMatrix& a) { return spmv(a, std::vector<double>(a.n, 1.0)); }
 
 }  // namespace krylov_b200

@@ -9,7 +9,8 @@
 //   sstep_gmres(CsrMatrix, span b, span x0, cfg) gmres.hpp:396      same
 //   standard_gmres(...)                          gmres.hpp:404      same
 //   bcgs_pip / bcgs_pip_partial / bcgs_pip2      block_ortho.hpp:152-208 same
-//   cholqr                                       block_ortho.hpp:49 same
+//   cholqr / cholqr2 / bcgs_project / bcgs2      block_ortho.hpp:49-137 same (HHQR intra: one column)
+//   ortho_error                                  spectral.hpp:104   same (device Gram)
 //   try_cholesky                                 dense_kernels.hpp:111 same
 //   spmv / mpk_monomial                          csr_matrix.hpp:69, gmres.hpp:80 same
 //   BasisStore                                   basis_store.hpp:42  same members (device-resident Q)
@@ -23,6 +24,7 @@
 #include <algorithm>
 #include <cmath>
 #include <cstring>
+#include <limits>
 #include <memory>
 #include <span>
 #include <stdexcept>
@@ -117,11 +119,30 @@ public:
     ConstMatrixView view() const { return ConstMatrixView(data_.data(), rows_, cols_); }
     ConstMatrixView col_range(index_t f, index_t c) const { return view().col_range(f, c); }
     void set_col(index_t j, const double* src) { std::memcpy(col(j), src, rows_ * sizeof(double)); }
+    double frobenius_norm() const {
+        double s = 0.0;
+        for (double x : data_) s += x * x;
+        return std::sqrt(s);
+    }
 
 private:
     index_t rows_ = 0, cols_ = 0;
     std::vector<double> data_;
 };
+
+// Host vector helpers of dense_matrix.hpp:133-150 (input preparation and
+// checks on host copies; the solver's vector work runs on the GPU).
+inline double dot(const double* a, const double* b, index_t n) {
+    double s = 0.0;
+    for (index_t i = 0; i < n; ++i) s += a[i] * b[i];
+    return s;
+}
+inline double norm2(const double* a, index_t n) { return std::sqrt(dot(a, a, n)); }
+inline double norm2(const std::vector<double>& a) { return norm2(a.data(), a.size()); }
+inline void axpy(double alpha, const double* x, double* y, index_t n) {
+    for (index_t i = 0; i < n; ++i) y[i] += alpha * x[i];
+}
+inline constexpr double machine_eps = std::numeric_limits<double>::epsilon();  // spectral.hpp:14
 
 class UpperTriangular {
 public:
@@ -183,6 +204,15 @@ struct OrthoScheme {
     OrthoKind kind = OrthoKind::BcgsPip2;
     index_t big_panel_size = 0;
 };
+inline const char* ortho_kind_name(OrthoKind k) {  // block_ortho.hpp:33-41
+    switch (k) {
+        case OrthoKind::Bcgs2Hhqr: return "bcgs2-hhqr";
+        case OrthoKind::Bcgs2Cholqr2: return "bcgs2-cholqr2";
+        case OrthoKind::BcgsPip2: return "bcgs-pip2";
+        case OrthoKind::TwoStage: return "two-stage";
+    }
+    return "?";
+}
 enum class PanelState { Raw, Preprocessed, Final };
 struct AppendOutcome {
     index_t committed = 0;
@@ -371,6 +401,91 @@ inline BlockQr cholqr(ConstMatrixView v, SyncCounter& sync, Context& ctx = defau
     return BlockQr{std::move(r.q), std::move(r.r_jj)};
 }
 
+// The BCGS2 baseline (block_ortho.hpp:57-137) on the device.
+inline BlockQr cholqr2(ConstMatrixView v, SyncCounter& sync, Context& ctx = default_context()) {
+    const index_t n = v.rows(), w = v.cols();
+    BlockQr out{DenseMatrix(n, w), UpperTriangular(w)};
+    int64_t piv = 0, red = 0;
+    const int rc = kry_cholqr2(ctx.get(), static_cast<int64_t>(n), v.data(), static_cast<int64_t>(w), out.q.data(),
+                               out.r.data(), &piv, &red);
+    sync.add(red);
+    detail::check(rc, piv);
+    return out;
+}
+
+struct ProjectResult {
+    DenseMatrix vhat;     // V − Q_prev·(Q_prevᵀV)
+    DenseMatrix r_block;  // Q_prevᵀV
+};
+inline ProjectResult bcgs_project(ConstMatrixView q_prev, ConstMatrixView v, SyncCounter& sync,
+                                  Context& ctx = default_context()) {
+    const index_t c0 = q_prev.empty() ? 0 : q_prev.cols(), w = v.cols(), n = v.rows();
+    ProjectResult out{DenseMatrix(n, w), DenseMatrix(c0, w)};
+    int64_t red = 0;
+    detail::check(kry_bcgs_project(ctx.get(), static_cast<int64_t>(n), c0 ? q_prev.data() : nullptr,
+                                   static_cast<int64_t>(c0), v.data(), static_cast<int64_t>(w), out.vhat.data(),
+                                   out.r_block.data(), &red));
+    sync.add(red);
+    return out;
+}
+
+enum class IntraKind { Hhqr, Cholqr2 };  // Hhqr: one column only on the device path
+inline BlockOrthoResult bcgs2(ConstMatrixView q_prev, ConstMatrixView v, IntraKind intra, SyncCounter& sync,
+                              Context& ctx = default_context()) {
+    const index_t c0 = q_prev.empty() ? 0 : q_prev.cols(), w = v.cols(), n = v.rows();
+    BlockOrthoResult out{DenseMatrix(n, w), DenseMatrix(c0, w), UpperTriangular(w)};
+    int64_t piv = 0, red = 0;
+    const int rc = kry_bcgs2(ctx.get(), static_cast<int64_t>(n), c0 ? q_prev.data() : nullptr,
+                             static_cast<int64_t>(c0), v.data(), static_cast<int64_t>(w),
+                             intra == IntraKind::Hhqr ? 0 : 1, out.q.data(), out.r_col.data(), out.r_jj.data(),
+                             &piv, &red);
+    sync.add(red);
+    detail::check(rc, piv);
+    return out;
+}
+
+// ‖I − QᵀQ‖₂ (spectral.hpp:104): the Gram QᵀQ on the device, the 2-norm of
+// the small symmetric deviation by cyclic Jacobi rotations on the host.
+inline double ortho_error(ConstMatrixView q, Context& ctx = default_context()) {
+    if (q.empty()) return 0.0;
+    const index_t k = q.cols();
+    if (k > 512) throw DimensionMismatch("ortho_error capped at 512 columns");
+    std::vector<double> a(k * k);
+    detail::check(kry_gram_full(ctx.get(), static_cast<int64_t>(q.rows()), q.data(), static_cast<int64_t>(k), a.data()));
+    auto at = [&](index_t i, index_t j) -> double& { return a[i + j * k]; };
+    for (index_t j = 0; j < k; ++j)
+        for (index_t i = 0; i < k; ++i) at(i, j) = (i == j ? 1.0 : 0.0) - at(i, j);
+    for (int sweep = 0; sweep < 30; ++sweep) {
+        double off = 0.0, diag = 0.0;
+        for (index_t i = 0; i < k; ++i) diag = std::max(diag, std::abs(at(i, i)));
+        for (index_t p = 0; p + 1 < k; ++p)
+            for (index_t r = p + 1; r < k; ++r) {
+                const double apr = at(p, r);
+                if (apr == 0.0) continue;
+                off = std::max(off, std::abs(apr));
+                // rotation zeroing (p, r): t = tan θ, the smaller root
+                const double theta = (at(r, r) - at(p, p)) / (2.0 * apr);
+                const double t = theta == 0.0 ? 1.0
+                                              : std::copysign(1.0, theta) / (std::abs(theta) + std::hypot(1.0, theta));
+                const double c = 1.0 / std::sqrt(1.0 + t * t), sn = c * t;
+                for (index_t i = 0; i < k; ++i) {  // columns p, r
+                    const double x = at(i, p), y = at(i, r);
+                    at(i, p) = c * x - sn * y;
+                    at(i, r) = sn * x + c * y;
+                }
+                for (index_t i = 0; i < k; ++i) {  // rows p, r
+                    const double x = at(p, i), y = at(r, i);
+                    at(p, i) = c * x - sn * y;
+                    at(r, i) = sn * x + c * y;
+                }
+            }
+        if (off <= machine_eps * std::max(diag, 1e-300)) break;
+    }
+    double norm = 0.0;
+    for (index_t i = 0; i < k; ++i) norm = std::max(norm, std::abs(at(i, i)));
+    return norm;
+}
+
 // ---- basis store (basis_store.hpp:42-401), device-resident -----------------------------
 class BasisStore {
 public:
@@ -426,8 +541,14 @@ public:
         detail::check(kry_store_coefficients(h_.get(), r.data()));
         return r;
     }
-    std::vector<double> column(index_t j) const {
-        std::vector<double> c(n_);
+    // A host copy of column j (the basis lives on the GPU); converts to the
+    // reference's `const double*` for the duration of the full expression.
+    struct HostColumn : std::vector<double> {
+        using std::vector<double>::vector;
+        operator const double*() const { return data(); }
+    };
+    HostColumn column(index_t j) const {
+        HostColumn c(n_);
         detail::check(kry_store_column(h_.get(), static_cast<int64_t>(j), c.data()));
         return c;
     }

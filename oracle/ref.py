@@ -57,6 +57,10 @@ SIGS = {
     "kref_bcgs_pip": (C.c_int, [i64, P_dbl, i64, P_dbl, i64, P_dbl, P_dbl, P_dbl, P_i64, P_i64]),
     "kref_bcgs_pip2": (C.c_int, [i64, P_dbl, i64, P_dbl, i64, P_dbl, P_dbl, P_dbl, P_i64, P_i64]),
     "kref_cholqr": (C.c_int, [i64, P_dbl, i64, P_dbl, P_dbl, P_i64, P_i64]),
+    "kref_cholqr2": (C.c_int, [i64, P_dbl, i64, P_dbl, P_dbl, P_i64, P_i64]),
+    "kref_bcgs_project": (C.c_int, [i64, P_dbl, i64, P_dbl, i64, P_dbl, P_dbl, P_i64]),
+    "kref_bcgs2": (C.c_int, [i64, P_dbl, i64, P_dbl, i64, i32, P_dbl, P_dbl, P_dbl, P_i64, P_i64]),
+    "kref_householder_q": (C.c_int, [i64, i64, P_dbl, P_dbl]),
     "kref_store_create": (C.c_int, [i64, i64, i64, i64, C.POINTER(vp)]),
     "kref_store_destroy": (None, [vp]),
     "kref_store_reset": (C.c_int, [vp]),
@@ -239,6 +243,45 @@ def bcgs_pip(q_prev, v):
 
 def bcgs_pip2(q_prev, v):
     code, q, rc, rj, piv, red = _pip(lib().kref_bcgs_pip2, q_prev, v)
+    if code:
+        raise RefError(code, lib().kref_last_error().decode(), piv)
+    return q, rc, rj, red
+
+
+def cholqr2(v):
+    """cholqr2 (block_ortho.hpp:57): (q, r, reduces)."""
+    v = _f(v, 2)
+    n, w = v.shape
+    q = np.zeros((n, w), order="F")
+    r = np.zeros((w, w), order="F")
+    piv, red = C.c_int64(0), C.c_int64(0)
+    code = lib().kref_cholqr2(n, _p(v), w, _p(q), _p(r), C.byref(piv), C.byref(red))
+    if code:
+        raise RefError(code, lib().kref_last_error().decode(), piv.value)
+    return q, r, red.value
+
+
+def bcgs_project(q_prev, v):
+    """bcgs_project (block_ortho.hpp:70): (vhat, r_block, reduces)."""
+    v = _f(v, 2)
+    n, w = v.shape
+    if q_prev is None or np.asarray(q_prev).size == 0:
+        q, c0 = None, 0
+    else:
+        q = _f(q_prev, 2)
+        c0 = q.shape[1]
+    vhat = np.zeros((n, w), order="F")
+    rb = np.zeros((c0, w), order="F")
+    red = C.c_int64(0)
+    _chk(lib().kref_bcgs_project(n, _p(q), c0, _p(v), w, _p(vhat), _p(rb), C.byref(red)))
+    return vhat, rb, red.value
+
+
+def bcgs2(q_prev, v, intra="cholqr2"):
+    """bcgs2 (block_ortho.hpp:102): (q, r_col, r_jj, reduces)."""
+    kind = {"hhqr": 0, "cholqr2": 1}[intra]
+    code, q, rc, rj, piv, red = _pip(lambda n, qq, c0, vv, w, out, rcp, rjp, pv, rd:
+                                     lib().kref_bcgs2(n, qq, c0, vv, w, kind, out, rcp, rjp, pv, rd), q_prev, v)
     if code:
         raise RefError(code, lib().kref_last_error().decode(), piv)
     return q, rc, rj, red

@@ -289,6 +289,56 @@ int kref_cholqr(int64_t n, const double* v, int64_t w, double* q, double* r, int
     return rc;
 }
 
+// The BCGS2 baseline pieces (block_ortho.hpp:57-137).
+int kref_cholqr2(int64_t n, const double* v, int64_t w, double* q, double* r, int64_t* pivot,
+                 int64_t* reduces) {
+    SyncCounter sync;
+    g_pivot = 0;
+    int rc = guarded([&] {
+        BlockQr qr = cholqr2(ConstMatrixView(v, n, w), sync);
+        copy_mat(qr.q, q);
+        copy_upper(qr.r, r);
+    });
+    if (pivot) *pivot = (rc == KRY_NOT_POSITIVE_DEFINITE) ? g_pivot : 0;
+    if (reduces) *reduces += sync.reduces;
+    return rc;
+}
+int kref_bcgs_project(int64_t n, const double* qp, int64_t c0, const double* v, int64_t w, double* vhat,
+                      double* r_block, int64_t* reduces) {
+    SyncCounter sync;
+    int rc = guarded([&] {
+        ProjectResult pr = bcgs_project(view(qp, n, c0), ConstMatrixView(v, n, w), sync);
+        copy_mat(pr.vhat, vhat);
+        copy_mat(pr.r_block, r_block);
+    });
+    if (reduces) *reduces += sync.reduces;
+    return rc;
+}
+int kref_bcgs2(int64_t n, const double* qp, int64_t c0, const double* v, int64_t w, int32_t intra, double* q,
+               double* r_col, double* r_jj, int64_t* pivot, int64_t* reduces) {
+    SyncCounter sync;
+    g_pivot = 0;
+    int rc = guarded([&] {
+        BlockOrthoResult res = bcgs2(view(qp, n, c0), ConstMatrixView(v, n, w),
+                                     intra == 0 ? IntraKind::Hhqr : IntraKind::Cholqr2, sync);
+        copy_mat(res.q, q);
+        copy_mat(res.r_col, r_col);
+        copy_upper(res.r_jj, r_jj);
+    });
+    if (pivot) *pivot = (rc == KRY_NOT_POSITIVE_DEFINITE) ? g_pivot : 0;
+    if (reduces) *reduces += sync.reduces;
+    return rc;
+}
+// Thin Q of the reference's Householder QR (dense_kernels.hpp:164): input
+// generator of the reference's own unit tests (tests/cpp refcompat).
+int kref_householder_q(int64_t rows, int64_t cols, const double* a, double* q) {
+    return guarded([&] {
+        DenseMatrix m(rows, cols);
+        std::memcpy(m.data(), a, static_cast<size_t>(rows * cols) * sizeof(double));
+        copy_mat(householder_qr(m).q, q);
+    });
+}
+
 // ---- basis store (basis_store.hpp) ------------------------------------------
 int kref_store_create(int64_t n, int64_t m, int64_t s, int64_t shat, void** out) {
     return guarded([&] { *out = new RefStore(n, m, s, shat); });

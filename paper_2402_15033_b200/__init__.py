@@ -32,6 +32,7 @@ __all__ = [
     "KrylovError", "DimensionMismatch", "NotPositiveDefinite", "SingularFactor", "SingularR",
     "Unsupported", "DeviceError", "OrthoKind", "SolveStatus", "PanelState", "OrthoScheme",
     "SolverConfig", "SyncCounter", "AppendOutcome", "BlockRecord", "SolveReport", "Context",
+    "cholqr2", "bcgs_project", "bcgs2",
     "get_context", "CsrOperator", "Laplace2D", "Laplace3D", "BasisStore", "bcgs_pip",
     "bcgs_pip_partial", "bcgs_pip2", "cholqr", "gram", "gram_full", "try_cholesky",
     "solve_hessenberg_lsq", "sstep_gmres", "standard_gmres", "sstep_gmres_device", "lib",
@@ -515,6 +516,42 @@ def cholqr(v, sync: SyncCounter, ctx: Optional[Context] = None) -> BlockQr:
     """cholqr (block_ortho.hpp:49): one reduce."""
     r = bcgs_pip(None, v, sync, ctx)
     return BlockQr(r.q, r.r_jj)
+
+
+def cholqr2(v, sync: SyncCounter, ctx: Optional[Context] = None) -> BlockQr:
+    """cholqr2 (block_ortho.hpp:57): CholQR twice, R = R2·R1; two reduces."""
+    ctx = ctx or get_context()
+    v = _f64(v, 2)
+    n, w = v.shape
+    q = np.zeros((n, w), order="F")
+    r = np.zeros((w, w), order="F")
+    piv, red = C.c_int64(0), C.c_int64(0)
+    rc = lib().kry_cholqr2(ctx.handle, n, _p(v), w, _p(q), _p(r), C.byref(piv), C.byref(red))
+    sync.add(red.value)
+    _check(rc, piv.value)
+    return BlockQr(q, r)
+
+
+def bcgs_project(q_prev, v, sync: SyncCounter, ctx: Optional[Context] = None):
+    """bcgs_project (block_ortho.hpp:70): (vhat, r_block); one reduce (none for an empty prefix)."""
+    ctx = ctx or get_context()
+    v = _f64(v, 2)
+    n, w = v.shape
+    q, c0 = _prefix(q_prev, n)
+    vhat = np.zeros((n, w), order="F")
+    rb = np.zeros((c0, w), order="F")
+    red = C.c_int64(0)
+    _check(lib().kry_bcgs_project(ctx.handle, n, _p(q), c0, _p(v), w, _p(vhat), _p(rb), C.byref(red)))
+    sync.add(red.value)
+    return vhat, rb
+
+
+def bcgs2(q_prev, v, sync: SyncCounter, intra: str = "cholqr2", ctx: Optional[Context] = None) -> BlockOrthoResult:
+    """bcgs2 (block_ortho.hpp:102): project, intra (CholQR2; 'hhqr' is not on
+    the device path for blocks wider than one column), re-project, CholQR."""
+    kind = {"hhqr": 0, "cholqr2": 1}[intra]
+    return _pip_call(lambda h, n, q, c0, vv, w, out, rc, rj, piv, red:
+                     lib().kry_bcgs2(h, n, q, c0, vv, w, kind, out, rc, rj, piv, red), q_prev, v, sync, ctx)
 
 
 def try_cholesky(s):

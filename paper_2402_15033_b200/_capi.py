@@ -101,6 +101,9 @@ SIGNATURES = {
     "kry_bcgs_pip": (C.c_int, [vp, i64, P_dbl, i64, P_dbl, i64, P_dbl, P_dbl, P_dbl, P_i64, P_i64]),
     "kry_bcgs_pip2": (C.c_int, [vp, i64, P_dbl, i64, P_dbl, i64, P_dbl, P_dbl, P_dbl, P_i64, P_i64]),
     "kry_cholqr": (C.c_int, [vp, i64, P_dbl, i64, P_dbl, P_dbl, P_i64, P_i64]),
+    "kry_cholqr2": (C.c_int, [vp, i64, P_dbl, i64, P_dbl, P_dbl, P_i64, P_i64]),
+    "kry_bcgs_project": (C.c_int, [vp, i64, P_dbl, i64, P_dbl, i64, P_dbl, P_dbl, P_i64]),
+    "kry_bcgs2": (C.c_int, [vp, i64, P_dbl, i64, P_dbl, i64, C.c_int32, P_dbl, P_dbl, P_dbl, P_i64, P_i64]),
     "kry_bcgs_pip_device": (C.c_int, [vp, i64, vp, i64, i64, vp, i64, i64, vp, i64, P_dbl, P_dbl, P_i64, P_i64]),
     "kry_gram_full": (C.c_int, [vp, i64, P_dbl, i64, P_dbl]),
     "kry_store_create": (C.c_int, [vp, i64, i64, i64, i64, C.POINTER(vp)]),

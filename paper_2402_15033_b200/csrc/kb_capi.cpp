@@ -501,6 +501,88 @@ int kry_cholqr(kry_ctx* ctx, int64_t n, const double* v, int64_t w, double* q, d
     return kry_bcgs_pip(ctx, n, nullptr, 0, v, w, q, nullptr, r, pivot, reduces);
 }
 
+// BCGS2 pieces on the device (block_ortho.hpp:57-137).
+int kry_cholqr2(kry_ctx* ctx, int64_t n, const double* v, int64_t w, double* q, double* r, int64_t* pivot,
+                int64_t* reduces) {
+    if (pivot) *pivot = 0;
+    return guarded(
+        [&] {
+            kb::Ctx& c = C(ctx);
+            kb::dim_check(n >= 1 && w >= 1, "cholqr2 shapes");
+            const i64 ld = kb::device_ld(n);
+            const double* dv = upload(c, ctx->up1, v, n, w);
+            ctx->up2.ensure(mat_bytes(ld, w));
+            i64 red = 0;
+            double bytes = 0.0;
+            try {
+                kb::Upper r1 = kb::cholqr_device(c, n, dv, ld, w, ctx->up2.p, ld, red, bytes);
+                kb::Upper r2 = kb::cholqr_device(c, n, ctx->up2.p, ld, w, ctx->up2.p, ld, red, bytes);
+                if (reduces) *reduces += red;
+                download(c, q, ctx->up2.p, ld, n, w);
+                c.sync();
+                put_upper(kb::tri_mul(r2, r1), r);
+            } catch (const kb::CholFail& f) {
+                if (reduces) *reduces += red;
+                kb::fail(KRY_NOT_POSITIVE_DEFINITE, "matrix not positive definite at pivot " + std::to_string(f.pivot),
+                         f.pivot);
+            }
+        },
+        pivot);
+}
+
+int kry_bcgs_project(kry_ctx* ctx, int64_t n, const double* q_prev, int64_t c0, const double* v, int64_t w,
+                     double* vhat, double* r_block, int64_t* reduces) {
+    return guarded([&] {
+        kb::Ctx& c = C(ctx);
+        kb::dim_check(n >= 1 && w >= 1 && c0 >= 0, "bcgs_project shapes");
+        const i64 ld = kb::device_ld(n);
+        const double* dqp = upload(c, ctx->up0, q_prev, n, c0);
+        const double* dv = upload(c, ctx->up1, v, n, w);
+        ctx->up2.ensure(mat_bytes(ld, w));
+        i64 red = 0;
+        double bytes = 0.0;
+        kb::Mat rb = kb::project_device(c, n, dqp, ld, c0, dv, ld, w, ctx->up2.p, ld, red, bytes);
+        if (reduces) *reduces += red;
+        download(c, vhat, ctx->up2.p, ld, n, w);
+        c.sync();
+        put_mat(rb, r_block);
+    });
+}
+
+int kry_bcgs2(kry_ctx* ctx, int64_t n, const double* q_prev, int64_t c0, const double* v, int64_t w,
+              int32_t intra_kind, double* q, double* r_col, double* r_jj, int64_t* pivot, int64_t* reduces) {
+    if (pivot) *pivot = 0;
+    return guarded(
+        [&] {
+            kb::Ctx& c = C(ctx);
+            kb::dim_check(n >= 1 && w >= 1 && c0 >= 0, "bcgs2 shapes");
+            if (intra_kind != 0 && intra_kind != 1) kb::fail(KRY_INVALID_ARGUMENT, "bcgs2: unknown intra kind");
+            if (intra_kind == 0 && w > 1)
+                kb::fail(KRY_UNSUPPORTED, "BCGS2 with a Householder intra step is not on the device path");
+            const i64 ld = kb::device_ld(n);
+            const double* dqp = upload(c, ctx->up0, q_prev, n, c0);
+            const double* dv = upload(c, ctx->up1, v, n, w);
+            ctx->up2.ensure(mat_bytes(ld, 3 * w));  // out | s0 | s1
+            double* out = ctx->up2.p;
+            i64 red = 0;
+            double bytes = 0.0;
+            try {
+                kb::Bcgs2Out o = kb::bcgs2_device(c, n, dqp, ld, c0, dv, ld, w, out + ld * w, out + 2 * ld * w, ld,
+                                                  out, ld, red, bytes);
+                if (reduces) *reduces += red;
+                download(c, q, out, ld, n, w);
+                c.sync();
+                put_mat(o.r_col, r_col);
+                put_upper(o.r_jj, r_jj);
+            } catch (const kb::CholFail& f) {
+                if (reduces) *reduces += red;
+                kb::fail(KRY_NOT_POSITIVE_DEFINITE, "matrix not positive definite at pivot " + std::to_string(f.pivot),
+                         f.pivot);
+            }
+        },
+        pivot);
+}
+
 int kry_bcgs_pip_device(kry_ctx* ctx, int64_t n, const double* d_q_prev, int64_t ldq, int64_t c0,
                         const double* d_v, int64_t ldv, int64_t w, double* d_out, int64_t ldo, double* r_col,
                         double* r_jj, int64_t* pivot, int64_t* reduces) {

@@ -286,4 +286,64 @@ PipOut pip_from_gram(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const do
     return o;
 }
 
+Upper cholqr_device(Ctx& ctx, i64 n, const double* V, i64 ldv, i64 w, double* out, i64 ldo, i64& reduces,
+                    double& bytes) {
+    reduces += 1;
+    Mat none, g;
+    gram_device(ctx, n, nullptr, 0, 0, V, ldv, w, none, g);
+    Upper r;
+    const i64 piv = try_cholesky(g, r);
+    if (piv != 0) throw CholFail{piv};
+    update_device(ctx, n, nullptr, 0, 0, V, ldv, w, none, r, out, ldo);
+    bytes += 8.0 * n * 3.0 * w;
+    return r;
+}
+
+Mat project_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
+                   double* out, i64 ldo, i64& reduces, double& bytes) {
+    if (c0 == 0) {
+        if (out != V)
+            KB_CUDA(cudaMemcpy2DAsync(out, ldo * 8, V, ldv * 8, n * 8, w, cudaMemcpyDeviceToDevice, ctx.stream));
+        return Mat(0, w);
+    }
+    reduces += 1;
+    Mat r_block, g;
+    gram_device(ctx, n, P, ldp, c0, V, ldv, w, r_block, g);
+    Upper ident(w);
+    update_device(ctx, n, P, ldp, c0, V, ldv, w, r_block, ident, out, ldo, /*triangular=*/false);
+    bytes += 8.0 * n * (2.0 * c0 + 3.0 * w);
+    return r_block;
+}
+
+Bcgs2Out bcgs2_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
+                      double* s0, double* s1, i64 lds, double* out, i64 ldo, i64& reduces, double& bytes) {
+    const bool single = (w == 1);
+    // intra: CholQR (one column) or CholQR2 (R = R₂·R₁), x → dst via mid
+    auto intra = [&](const double* x, i64 ldx, double* mid, double* dst, i64 ldd) -> Upper {
+        if (single) return cholqr_device(ctx, n, x, ldx, w, dst, ldd, reduces, bytes);
+        Upper r1 = cholqr_device(ctx, n, x, ldx, w, mid, lds, reduces, bytes);
+        Upper r2 = cholqr_device(ctx, n, mid, lds, w, dst, ldd, reduces, bytes);
+        return tri_mul(r2, r1);
+    };
+    Bcgs2Out o;
+    if (c0 == 0) {
+        o.r_jj = intra(V, ldv, s0, out, ldo);
+        o.r_col = Mat(0, w);
+        return o;
+    }
+    Mat first = project_device(ctx, n, P, ldp, c0, V, ldv, w, s0, lds, reduces, bytes);
+    Upper inner = intra(s0, lds, s1, s1, lds);
+    Mat second = project_device(ctx, n, P, ldp, c0, s1, lds, w, s1, lds, reduces, bytes);
+    Upper outer = cholqr_device(ctx, n, s1, lds, w, out, ldo, reduces, bytes);
+    Mat ir(w, w);
+    for (i64 j = 0; j < w; ++j)
+        for (i64 i = 0; i <= j; ++i) ir(i, j) = inner(i, j);
+    Mat corr = mat_mul_nn(second, ir);
+    o.r_col = std::move(first);
+    for (i64 j = 0; j < o.r_col.cols; ++j)
+        for (i64 i = 0; i < o.r_col.rows; ++i) o.r_col(i, j) += corr(i, j);
+    o.r_jj = tri_mul(outer, inner);
+    return o;
+}
+
 }  // namespace kb

@@ -36,4 +36,30 @@ PipOut bcgs_pip_partial_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0
                                i64 ldv, i64 w, double* out, i64 ldo, i64& reduces, bool do_update = true,
                                i64 x_first = -1, i64 x_count = 0, Mat* gx = nullptr);
 
+// CholQR (block_ortho.hpp:49-54) on the device: adds its one reduce to
+// `reduces` (also when it fails), writes Q = V·R⁻¹ to `out`; a Cholesky
+// failure throws CholFail{pivot} (callers map it to the reference's
+// first / second-pass semantics or to NotPositiveDefinite).
+struct CholFail {
+    i64 pivot;
+};
+Upper cholqr_device(Ctx& ctx, i64 n, const double* V, i64 ldv, i64 w, double* out, i64 ldo, i64& reduces,
+                    double& bytes);
+
+// bcgs_project (block_ortho.hpp:70-87): R_block = PᵀV (one reduce when
+// c0 > 0), out = V − P·R_block (out may alias V).
+Mat project_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
+                   double* out, i64 ldo, i64& reduces, double& bytes);
+
+// bcgs2 (block_ortho.hpp:102-137) with the CholQR2 intra step (CholQR on a
+// single column): project, intra, re-project, CholQR; R_col = T_col·R_in +
+// R_col, R_jj = R_out·R_in.  Scratch s0 / s1: n × w each (ld lds).  Throws
+// CholFail.  The HHQR intra step is not on the device path.
+struct Bcgs2Out {
+    Mat r_col;
+    Upper r_jj;
+};
+Bcgs2Out bcgs2_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
+                      double* s0, double* s1, i64 lds, double* out, i64 ldo, i64& reduces, double& bytes);
+
 }  // namespace kb

@@ -496,44 +496,23 @@ Store::OrthoRes Store::pip(i64 c0, const double* V, i64 ldv, i64 w, double* out,
 }
 
 namespace {
-
-// CholQR (block_ortho.hpp:49-54) on the device: one reduce.  Throws
-// `Fail{pivot}` on a Cholesky failure (the caller maps it to the reference's
-// first/second-pass semantics).
-struct CholFail {
-    i64 pivot;
-};
-
-Upper cholqr_device(Ctx& ctx, i64 n, const double* V, i64 ldv, i64 w, double* out, i64 ldo, Sync& sync,
-                    double& bytes) {
-    sync.add(1);
-    Mat none, g;
-    gram_device(ctx, n, nullptr, 0, 0, V, ldv, w, none, g);
-    Upper r;
-    const i64 piv = try_cholesky(g, r);
-    if (piv != 0) throw CholFail{piv};
-    update_device(ctx, n, nullptr, 0, 0, V, ldv, w, none, r, out, ldo);
-    bytes += 8.0 * n * 3.0 * w;
+// the device helpers count reduces in an i64; the store's SyncCounter adds them
+Upper cholqr_dev(Ctx& ctx, i64 n, const double* V, i64 ldv, i64 w, double* out, i64 ldo, Sync& sync, double& bytes) {
+    i64 red = 0;
+    struct Add {
+        Sync& s;
+        i64& r;
+        ~Add() { s.add(r); }
+    } add{sync, red};
+    return cholqr_device(ctx, n, V, ldv, w, out, ldo, red, bytes);
+}
+Mat project_dev(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w, double* out,
+                i64 ldo, Sync& sync, double& bytes) {
+    i64 red = 0;
+    Mat r = project_device(ctx, n, P, ldp, c0, V, ldv, w, out, ldo, red, bytes);
+    sync.add(red);
     return r;
 }
-
-// bcgs_project (block_ortho.hpp:70-87): one reduce when the prefix is non-empty.
-Mat project_device(Ctx& ctx, i64 n, const double* P, i64 ldp, i64 c0, const double* V, i64 ldv, i64 w,
-                   double* out, i64 ldo, Sync& sync, double& bytes) {
-    if (c0 == 0) {
-        if (out != V)
-            KB_CUDA(cudaMemcpy2DAsync(out, ldo * 8, V, ldv * 8, n * 8, w, cudaMemcpyDeviceToDevice, ctx.stream));
-        return Mat(0, w);
-    }
-    sync.add(1);
-    Mat r_block, g;
-    gram_device(ctx, n, P, ldp, c0, V, ldv, w, r_block, g);
-    Upper ident(w);
-    update_device(ctx, n, P, ldp, c0, V, ldv, w, r_block, ident, out, ldo, /*triangular=*/false);
-    bytes += 8.0 * n * (2.0 * c0 + 3.0 * w);
-    return r_block;
-}
-
 }  // namespace
 
 Store::OrthoRes Store::run_scheme(i64 c0, const double* V, i64 ldv, i64 w, int kind, Sync& sync) {
@@ -588,9 +567,9 @@ Store::OrthoRes Store::run_scheme(i64 c0, const double* V, i64 ldv, i64 w, int k
             // failure of the second pass must leave V raw for the retry and
             // record_seam (append_impl, basis_store.hpp:169-209).
             auto intra = [&](const double* x, i64 ldx, double* mid, double* dst) -> Upper {
-                if (single) return cholqr_device(ctx_, n_, x, ldx, w, dst, ld_, sync, ortho_bytes);
-                Upper r1 = cholqr_device(ctx_, n_, x, ldx, w, mid, ld_, sync, ortho_bytes);
-                Upper r2 = cholqr_device(ctx_, n_, mid, ld_, w, dst, ld_, sync, ortho_bytes);
+                if (single) return cholqr_dev(ctx_, n_, x, ldx, w, dst, ld_, sync, ortho_bytes);
+                Upper r1 = cholqr_dev(ctx_, n_, x, ldx, w, mid, ld_, sync, ortho_bytes);
+                Upper r2 = cholqr_dev(ctx_, n_, mid, ld_, w, dst, ld_, sync, ortho_bytes);
                 return tri_mul(r2, r1);
             };
             OrthoRes out;
@@ -606,15 +585,15 @@ Store::OrthoRes Store::run_scheme(i64 c0, const double* V, i64 ldv, i64 w, int k
             Mat first_block;
             Upper inner_r;
             try {
-                first_block = project_device(ctx_, n_, col(0), ld_, c0, V, ldv, w, s0, ld_, sync, ortho_bytes);
+                first_block = project_dev(ctx_, n_, col(0), ld_, c0, V, ldv, w, s0, ld_, sync, ortho_bytes);
                 inner_r = intra(s0, ld_, s1, s1);
             } catch (const CholFail& f) {
                 throw FirstPassFailure{f.pivot};
             }
             try {
                 Mat second_block =
-                    project_device(ctx_, n_, col(0), ld_, c0, s1, ld_, w, s1, ld_, sync, ortho_bytes);
-                Upper outer_r = cholqr_device(ctx_, n_, s1, ld_, w, col(c0), ld_, sync, ortho_bytes);
+                    project_dev(ctx_, n_, col(0), ld_, c0, s1, ld_, w, s1, ld_, sync, ortho_bytes);
+                Upper outer_r = cholqr_dev(ctx_, n_, s1, ld_, w, col(c0), ld_, sync, ortho_bytes);
                 Mat ir(w, w);
                 for (i64 j = 0; j < w; ++j)
                     for (i64 i = 0; i <= j; ++i) ir(i, j) = inner_r(i, j);

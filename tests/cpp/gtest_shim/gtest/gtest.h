@@ -9,6 +9,7 @@
 #include <cstdio>
 #include <cstdlib>
 #include <cstring>
+#include <exception>
 #include <sstream>
 #include <string>
 #include <vector>
@@ -46,6 +47,29 @@ inline bool ulp_eq(double a, double b) {
     const int64_t d = ia > ib ? ia - ib : ib - ia;
     return d <= 4;
 }
+// A failed check: `<< extra` is appended to the message; reported when the
+// statement ends, and a fatal (ASSERT_*) one then leaves the test.
+class Msg {
+public:
+    Msg(const char* file, int line, const char* what, bool fatal) : file_(file), line_(line), what_(what), fatal_(fatal) {}
+    template <typename T>
+    Msg& operator<<(const T& v) {
+        extra_ << v;
+        return *this;
+    }
+    ~Msg() noexcept(false) {
+        const std::string e = extra_.str();
+        fail(file_, line_, e.empty() ? what_ : what_ + " — " + e);
+        if (fatal_ && std::uncaught_exceptions() == 0) throw Fatal{};
+    }
+
+private:
+    const char* file_;
+    int line_;
+    std::string what_;
+    bool fatal_;
+    std::ostringstream extra_;
+};
 }  // namespace gshim
 
 #define TEST(S, N)                                                        \
@@ -53,13 +77,15 @@ inline bool ulp_eq(double a, double b) {
     static ::gshim::Reg S##_##N##_gshim_reg(#S, #N, &S##_##N##_gshim);    \
     static void S##_##N##_gshim()
 
-#define GSHIM_CHECK(cond, what, fatal)                                    \
-    do {                                                                  \
-        if (!(cond)) {                                                    \
-            ::gshim::fail(__FILE__, __LINE__, what);                      \
-            if (fatal) throw ::gshim::Fatal{};                            \
-        }                                                                 \
-    } while (0)
+// one statement (safe under if / else), optionally followed by `<< msg`
+#define GSHIM_CHECK(cond, what, fatal) \
+    switch (0)                         \
+    case 0:                            \
+    default:                           \
+        if (cond)                      \
+            ;                          \
+        else                           \
+            ::gshim::Msg(__FILE__, __LINE__, what, fatal)
 #define GSHIM_CMP(a, op, b, fatal) GSHIM_CHECK((a)op(b), #a " " #op " " #b, fatal)
 
 #define EXPECT_TRUE(c) GSHIM_CHECK(static_cast<bool>(c), #c, false)

@@ -38,3 +38,32 @@ def test_reference_sparse_core_tests_pass_against_the_dropin():
     p = subprocess.run([exe], capture_output=True, text=True, timeout=600)
     assert p.returncode == 0, p.stdout + p.stderr
     assert "13 tests, 13 passed, 0 failed" in p.stdout, p.stdout
+
+
+# The reference's own failures (the first-pass error
+# window of CholQr2.FirstPassErrorTracksKappaSquared fails in the reference
+# itself) and the one scheme the device path does not carry (BCGS2 with a
+# Householder intra step: HHQR out of scope).  The reference's four
+# SEGV tests (two-stage store, Appendix A.1) must pass here.
+BLOCK_ORTHO_ALLOWED_FAILURES = {"CholQr2.FirstPassErrorTracksKappaSquared", "Bcgs2.HhqrIntraSyncAccounting"}
+
+
+def test_reference_block_ortho_tests_compiled_unchanged():
+    """The reference's own tests/test_block_ortho.cpp (CholQR / CholQR2, BCGS
+    project, BCGS2, BCGS-PIP / PIP2, the BasisStore incl. two-stage), compiled
+    unchanged against include/krylov_b200 through tests/cpp/refcompat; every
+    orthogonalization and store call runs on the GPU, the test matrices come
+    from the reference's own generators (oracle/_ref)."""
+    exe = os.path.join(ROOT, "tests", "cpp", "ref_block_ortho")
+    if not os.path.exists(exe):
+        pytest.skip("ref_block_ortho not built (needs /root/reference at build time)")
+    p = subprocess.run([exe], capture_output=True, text=True, timeout=1200)
+    failed = {ln.split("]", 1)[1].strip() for ln in p.stdout.splitlines() if ln.startswith("[ FAIL ]")}
+    passed = {ln.split("]", 1)[1].strip() for ln in p.stdout.splitlines() if ln.startswith("[  OK  ]")}
+    assert "20 tests," in p.stdout, p.stdout + p.stderr
+    assert failed <= BLOCK_ORTHO_ALLOWED_FAILURES, p.stdout
+    for must in ["BasisStore.TwoStageEqualsPip2WhenBigPanelIsPanel", "BasisStore.TwoStageSyncCounts",
+                 "BasisStore.PartialBigPanelFinalizedAtActualWidth", "BasisStore.StatesTrackTwoStageLifecycle",
+                 "BasisStore.RawSequenceReconstruction", "Bcgs2.GluedAccumulationStaysOrthogonal",
+                 "BcgsPip2.MonotoneFailure"]:
+        assert must in passed, p.stdout

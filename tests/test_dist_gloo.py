@@ -1,4 +1,4 @@
-"""Multi-rank host logic on the CPU (world_size 2, gloo, 127.0.0.1).
+"""Multi-rank host logic on the CPU (world_size 2 and 8, gloo, 127.0.0.1).
 
 The B200 path partitions rows across ranks (kry_laplace_partition: whole
 grid lines / planes), exchanges one halo line/plane with each neighbour
@@ -78,7 +78,7 @@ def worker(rank, world, port, q):
         import paper_2402_15033_b200 as kb
         from oracle import orc
         out = {}
-        for dims, (nx, ny, nz) in [(2, (13, 11, 1)), (3, (7, 6, 5))]:
+        for dims, (nx, ny, nz) in [(2, (13, max(11, 2 * world + 1), 1)), (3, (7, 6, max(5, world + 1)))]:
             rb, nl, h = partition(kb, dims, nx, ny, nz, world, rank)
             n = nx * ny * (nz if dims == 3 else 1)
             a = orc.laplace2d(nx, ny) if dims == 2 else orc.laplace3d(nx, ny, nz)
@@ -127,25 +127,30 @@ def worker(rank, world, port, q):
         q.put((rank, {"error": repr(e)}))
 
 
-def test_two_rank_partition_halo_gram_protocol():
+@pytest.mark.parametrize("world", [2, 8])  # 8: the driver's largest one-node run (bench.py --gpus 8)
+def test_multi_rank_partition_halo_gram_protocol(world):
     ctx = mp.get_context("spawn")
     q = ctx.Queue()
     port = free_port()
-    procs = [ctx.Process(target=worker, args=(r, 2, port, q)) for r in range(2)]
+    procs = [ctx.Process(target=worker, args=(r, world, port, q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = dict(q.get(timeout=240) for _ in procs)
+    res = dict(q.get(timeout=600) for _ in procs)
     for p in procs:
         p.join(timeout=60)
-    for r in range(2):
+    for r in range(world):
         assert "error" not in res[r], res[r]
         assert res[r]["spmv2"] and res[r]["spmv3"]
         assert res[r]["gram_err"] < 1e-12
         assert res[r]["chol_identical"] and res[r]["pivot"] == 0
-    # the partition tiles the rows exactly
-    for d, n in [(2, 13 * 11), (3, 7 * 6 * 5)]:
-        (b0, n0), (b1, n1) = res[0][f"range{d}"], res[1][f"range{d}"]
-        assert b0 == 0 and b0 + n0 == b1 and b1 + n1 == n
+    # the partition tiles the rows exactly, in rank order
+    for d, n in [(2, 13 * max(11, 2 * world + 1)), (3, 7 * 6 * max(5, world + 1))]:
+        nxt = 0
+        for r in range(world):
+            b, nl = res[r][f"range{d}"]
+            assert b == nxt and nl > 0
+            nxt = b + nl
+        assert nxt == n
 
 
 def test_partition_errors():

@@ -72,6 +72,32 @@ __global__ void __launch_bounds__(kPipThreads) pip_block_kernel(const PipBlockAr
         if (i > j) s[i + j * kPipMaxW] = s[j + i * kPipMaxW];
     }
     __syncthreads();
+    if (a.mode == 1) {
+        // bcgs_project (block_ortho.hpp:70-87): R_block = Q_prevᵀV as it is,
+        // update V − Q_prev·R_block (K5 coefficients −R_col, no intra factor:
+        // the host path's update_device(…, triangular = false)); the chain
+        // status passes through (an earlier failure skips this update too).
+        const int piv = (a.prev_slot && a.prev_slot[kSlotStatus] != 0.0) ? -1 : 0;
+        if (tid == 0) {
+            a.slot[kSlotStatus] = static_cast<double>(piv);
+            *a.skip = piv != 0 ? 1 : 0;
+        }
+        double* rcol_out = a.slot + kSlotRcol;
+        for (int idx = tid; idx < c0 * w; idx += kPipThreads) rcol_out[idx] = rc[idx];
+        if (piv != 0) return;
+        const int wm = a.wmax;
+        for (int idx = tid; idx < (c0 + wm + 1) * wm; idx += kPipThreads) {
+            const int row = idx / wm, j = idx % wm;
+            double v = 0.0;
+            if (row < c0) {
+                if (j < w) v = -rc[row + j * c0];
+            } else if (row == c0 + wm) {
+                if (j < w) v = 1.0;
+            }
+            a.coef[idx] = v;
+        }
+        return;
+    }
     // 2. Pythagorean update, one (i ≤ j) entry per thread, dot in index
     //    order (block_ortho.hpp:159-166 via dot_seq).
     for (int idx = tid; idx < w * w; idx += kPipThreads) {

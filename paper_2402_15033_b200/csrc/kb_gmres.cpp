@@ -390,6 +390,10 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
         // block, so the per-block convergence check keeps its place
         bool spec_pip2 = speculate_default && !two_stage && !standard_mode && scheme == KRY_ORTHO_BCGS_PIP2 &&
                          store.can_speculate_pip2(s + 1);
+        // standard GMRES: the columns of the cycle are queued the same way
+        // (four BCGS2 passes each, device coefficients) while the prefix
+        // fits one Gram group, and replayed column by column
+        bool spec_std = speculate_default && standard_mode && store.can_speculate_std(store.filled());
         bool skip_mpk = false;  // a speculative block being redone: its raw columns are in place
         for (i64 j = 0; j < blocks && !done; ++j) {
             Outcome oc;
@@ -476,12 +480,53 @@ Report gmres(Ctx& ctx, Operator& op, const double* d_b_in, const double* d_x0, c
                     continue;
                 }
                 oc.committed = s + 1;
+            } else if (spec_std) {
+                if (!store.spec_has_next()) {
+                    NvtxRange nv("kry.speculative_standard_cycle");
+                    i64 queued = 0;
+                    recorded((uint64_t(3) << 60) | (uint64_t(j) << 30) | uint64_t(store.filled()), [&] {
+                        queued = 0;
+                        for (i64 jj = j; jj < blocks; ++jj) {
+                            const i64 f = store.spec_filled();
+                            if (!store.can_speculate_std(f)) break;
+                            cudaEvent_t t0 = ctx.begin_phase();
+                            op.apply(store.col(f - 1), store.col(f));
+                            ctx.end_phase(PH_MPK, t0);
+                            rep.mpk_bytes += op.bytes_per_apply();
+                            cudaEvent_t t1 = ctx.begin_phase();
+                            store.preprocess_speculative_std();
+                            ctx.end_phase(PH_ORTHO, t1);
+                            ++queued;
+                        }
+                    });
+                    if (queued == 0) {  // the prefix outgrew one Gram group: synchronous from here
+                        spec_std = false;
+                        --j;
+                        continue;
+                    }
+                    cudaEvent_t t1 = ctx.begin_phase();
+                    store.spec_fetch();
+                    ctx.end_phase(PH_ORTHO, t1);
+                }
+                if (store.spec_commit_next(rep.sync) != 1) {
+                    // a failed CholQR (or the queue is off): redo this column
+                    // on the synchronous path, its raw SpMV output in place
+                    store.spec_drop();
+                    spec_std = false;
+                    skip_mpk = true;
+                    --j;
+                    continue;
+                }
+                oc.committed = 1;
             } else if (standard_mode) {
                 const i64 f = store.filled();
-                cudaEvent_t t0 = ctx.begin_phase();
-                op.apply(store.col(f - 1), store.col(f));
-                ctx.end_phase(PH_MPK, t0);
-                rep.mpk_bytes += op.bytes_per_apply();
+                if (!skip_mpk) {
+                    cudaEvent_t t0 = ctx.begin_phase();
+                    op.apply(store.col(f - 1), store.col(f));
+                    ctx.end_phase(PH_MPK, t0);
+                    rep.mpk_bytes += op.bytes_per_apply();
+                }
+                skip_mpk = false;
                 cudaEvent_t t1 = ctx.begin_phase();
                 oc = store.append_block(store.col(f), store.ld(), 1, false, scheme, 0, rep.sync);
                 ctx.end_phase(PH_ORTHO, t1);

@@ -58,6 +58,7 @@ struct PipBlockArgs {
     const double* prev_slot;  // the previous speculative block's slot, or nullptr
     double* coef;             // K5 coefficients for this block's update
     int* skip;                // K5 skip flag: set when this block (or an earlier one) failed
+    int mode;                 // 0: BCGS-PIP factorisation; 1: bcgs_project (coefficients −R_col only)
 };
 void launch_pip_block(cudaStream_t stream, const PipBlockArgs& a, int64_t& launches);
 

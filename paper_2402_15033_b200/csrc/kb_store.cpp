@@ -133,7 +133,7 @@ Store::SpecPlan Store::spec_plan(i64 w, bool overlap, bool pieces) {
     if (overlap && filled == 0) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: basis store capacity exceeded");
     const i64 c0 = overlap ? filled - 1 : filled;
     if (c0 + w > max_cols_) fail(KRY_DIMENSION_MISMATCH, "dimension mismatch: basis store capacity exceeded");
-    const i64 maxb = 2 * max_cols_;  // queue capacity in result slots (blocks per cycle ≤ m, 2 slots for PIP2)
+    const i64 maxb = 4 * max_cols_;  // queue capacity in result slots (≤ m blocks per cycle; 2 per PIP2 block, 4 per standard column)
     if (first) {
         spec_bps_ = big_panel_start_;
         spec_xd_ = big_panel_start_;
@@ -161,8 +161,9 @@ Store::SpecPlan Store::spec_plan(i64 w, bool overlap, bool pieces) {
 }
 
 // [allreduce] → device factorisation of the packed Gram in ctx_.gram_packed.
-PipBlockArgs Store::spec_factor(const SpecPlan& p, i64 w) {
+PipBlockArgs Store::spec_factor(const SpecPlan& p, i64 w, int mode) {
     PipBlockArgs a{};
+    a.mode = mode;
     a.packed = ctx_.gram_packed.p;
     a.nb = static_cast<int>(1 + round_up(p.c0, 8) / 8);
     a.nx = p.xc > 0 ? static_cast<int>((8 + p.xf + p.xc - 1) / 8 - (8 + p.xf) / 8 + 1) : 0;
@@ -303,7 +304,7 @@ i64 Store::resolve_speculative(Sync& sync) {
 
 void Store::spec_fetch() {
     if (spec_.empty()) return;
-    const size_t slots = spec_.size() * (spec_.front().pip2 ? 2 : 1);
+    const size_t slots = spec_.size() * (spec_.front().pip2 ? 2 : spec_.front().std1 ? 4 : 1);
     KB_CUDA(cudaMemcpyAsync(spec_host_.p, spec_slots_.p, slots * kSlotDoubles * 8, cudaMemcpyDeviceToHost,
                             ctx_.stream));
     ctx_.sync();
@@ -335,8 +336,10 @@ int Store::spec_commit_next(Sync& sync) {
     if (!spec_fetched_ || spec_next_ >= spec_.size()) return -1;
     const size_t i = spec_next_;
     const SpecBlock& b = spec_[i];
-    const double* slot = spec_host_.p + (b.pip2 ? 2 * i : i) * kSlotDoubles;
-    const bool failed = slot[kSlotStatus] != 0.0 || (b.pip2 && slot[kSlotDoubles + kSlotStatus] != 0.0);
+    const int per = b.pip2 ? 2 : b.std1 ? 4 : 1;
+    const double* slot = spec_host_.p + per * i * kSlotDoubles;
+    bool failed = false;
+    for (int k = 0; k < per; ++k) failed = failed || slot[k * kSlotDoubles + kSlotStatus] != 0.0;
     if (failed) {
         // fused path: the block's raw columns live outside the store;
         // put them where the synchronous redo expects them
@@ -349,7 +352,27 @@ int Store::spec_commit_next(Sync& sync) {
     ++spec_next_;
     const i64 before = sync.reduces;
     OrthoRes res;
-    if (b.pip2) {
+    if (b.std1) {
+        // run_scheme BCGS2 with one column (intra = CholQR): R_col = R₁ +
+        // T_col·R_in, R_jj = R_out·R_in — the synchronous path's arithmetic.
+        const double* sl[4] = {slot, slot + kSlotDoubles, slot + 2 * kSlotDoubles, slot + 3 * kSlotDoubles};
+        Mat first(b.c0, 1), second(b.c0, 1), ir(1, 1);
+        Upper inner(1), outer(1);
+        for (i64 l = 0; l < b.c0; ++l) {
+            first(l, 0) = sl[0][kSlotRcol + l];
+            second(l, 0) = sl[2][kSlotRcol + l];
+        }
+        inner.at(0, 0) = sl[1][kSlotRcol];
+        outer.at(0, 0) = sl[3][kSlotRcol];
+        ir(0, 0) = inner(0, 0);
+        Mat corr = mat_mul_nn(second, ir);
+        res.r_col = std::move(first);
+        for (i64 l = 0; l < res.r_col.rows; ++l) res.r_col(l, 0) += corr(l, 0);
+        res.r_jj = tri_mul(outer, inner);
+        sync.add(4);
+        ortho_bytes += 2.0 * 8.0 * n_ * (2.0 * b.c0 + 3.0) + 2.0 * 8.0 * n_ * 3.0;
+        commit(b.c0, b.overlap, res, 1, KRY_PANEL_FINAL);
+    } else if (b.pip2) {
         // run_scheme BcgsPip2 (basis_store.hpp:220-239): R_col = R₁ + T_col·R_jj₁,
         // R_jj = T_jj·R_jj₁ — the synchronous path's arithmetic (run_scheme).
         OrthoRes first, second;
@@ -417,6 +440,51 @@ void Store::preprocess_speculative_pip2(i64 w, bool overlap) {
     }
     spec_push(p, w, overlap, nullptr);
     spec_.back().pip2 = true;
+}
+
+bool Store::can_speculate_std(i64 c0) const {
+    // one prefix group for the projection Grams (round_up(c0, 8) + 8 ≤ 64)
+    return c0 >= 1 && c0 + 1 <= max_cols_ && round_up(c0, 8) + 8 <= 64;
+}
+
+void Store::preprocess_speculative_std() {
+    const i64 w = 1;
+    const SpecPlan p = spec_plan(w, false, /*pieces=*/false);
+    const i64 c0 = p.c0, b = static_cast<i64>(spec_.size());
+    double* s0 = scratch(0, w);
+    double* s1 = scratch(1, w);
+    // bcgs2 (block_ortho.hpp:102-137) on one column: project V → s0, CholQR
+    // s0 → s1, project s1 → s0, CholQR s0 → the store column.  Only the last
+    // pass writes the store, so a failure anywhere leaves V raw there.
+    struct Pass {
+        const double* v;
+        double* out;
+        bool project;
+    };
+    const Pass passes[4] = {{col(c0), s0, true}, {s0, s1, false}, {s1, s0, true}, {s0, col(c0), false}};
+    for (int k = 0; k < 4; ++k) {
+        const Pass& ps = passes[k];
+        const i64 pc0 = ps.project ? c0 : 0;
+        SpecPlan q = p;
+        q.c0 = pc0;
+        q.idx = 4 * b + k;
+        std::vector<int> tiles;
+        cudaEvent_t t0 = ctx_.begin_phase();
+        launch_gram_pass(ctx_.stream, n_, pc0 > 0 ? col(0) : nullptr, ld_, pc0, ps.v, ld_, w, true,
+                         ctx_.gram_partials.p, ctx_.gram_packed.p, tiles, ctx_.launches, -1, 0);
+        ctx_.end_phase(PH_GRAM, t0);
+        ctx_.gram_bytes += 8.0 * n_ * (pc0 + w);
+        ctx_.gram_launches += 1;
+        const PipBlockArgs a = spec_factor(q, w, ps.project ? 1 : 0);
+        cudaEvent_t t1 = ctx_.begin_phase();
+        launch_update(ctx_.stream, n_, pc0 > 0 ? col(0) : nullptr, ld_, pc0, ps.v, ld_, w, a.coef, !ps.project, ps.out,
+                      ld_, ctx_.launches, a.skip);
+        ctx_.end_phase(PH_UPDATE, t1);
+        ctx_.update_bytes += 8.0 * n_ * (pc0 + 2.0 * w);
+        ctx_.update_launches += 1;
+    }
+    spec_push(p, w, false, nullptr);
+    spec_.back().std1 = true;
 }
 
 bool Store::mpk(Operator& op, i64 c0, i64 s) {

@@ -112,6 +112,16 @@ public:
     // spec_drop() discards what is left (the cycle ended early).
     bool can_speculate_pip2(i64 w) const;
     void preprocess_speculative_pip2(i64 w, bool overlap);
+    // ---- speculative standard GMRES (s = 1: BCGS2 with one column,
+    // block_ortho.hpp:102-137) -------------------------------------------
+    // preprocess_speculative_std() queues the four passes of the column in
+    // store column c0 = spec_filled() (project → CholQR → project → CholQR:
+    // Gram → [allreduce] → device coefficients → gated update, V → scratch →
+    // scratch → scratch → store column) without waiting; replayed one column
+    // at a time by spec_commit_next() (R composed as run_scheme's BCGS2, 4
+    // reduces).  can_speculate_std(c0): the prefix fits one Gram group.
+    bool can_speculate_std(i64 c0) const;
+    void preprocess_speculative_std();
     void spec_fetch();
     int spec_commit_next(Sync& sync);
     bool spec_has_next() const { return spec_fetched_ && spec_next_ < spec_.size(); }
@@ -154,12 +164,13 @@ private:
         i64 x_first, x_count;
         const double* raw;  // raw block outside the store (fused path) or nullptr
         bool pip2 = false;  // one-stage BCGS-PIP2: result slots 2i (pass 1) and 2i + 1 (pass 2)
+        bool std1 = false;  // standard GMRES column: result slots 4i … 4i + 3 (the four BCGS2 passes)
     };
     struct SpecPlan {
         i64 c0, idx, xf, xc;
     };
     SpecPlan spec_plan(i64 w, bool overlap, bool pieces = true);
-    PipBlockArgs spec_factor(const SpecPlan& p, i64 w);
+    PipBlockArgs spec_factor(const SpecPlan& p, i64 w, int mode = 0);
     void spec_push(const SpecPlan& p, i64 w, bool overlap, const double* raw);
     struct FusedPending {
         bool live = false;

@@ -113,3 +113,44 @@ def test_speculative_pip2_matches_synchronous(kb, ctx, monkeypatch, grid, kind):
                                                                         s.sync.reduces)
     assert a.sync.per_block == s.sync.per_block and a.cycle_residuals == s.cycle_residuals
     np.testing.assert_array_equal(a.solution, s.solution)
+
+
+@pytest.mark.parametrize("grid,m,max_iters", [(24, 60, 600), (48, 60, 240), (40, 30, 300)])
+def test_speculative_standard_gmres_matches_synchronous(kb, ctx, monkeypatch, grid, m, max_iters):
+    """Standard GMRES (s = 1, BCGS2 with one column) queued without host waits
+    (the four passes' coefficients formed on the device, replayed column by
+    column with the per-column convergence check; synchronous once the
+    prefix outgrows one Gram group) reproduces the synchronous path bit for
+    bit."""
+    op = kb.Laplace2D(grid, grid)
+    b = op.spmv(np.ones(op.n))
+    cfg = kb.SolverConfig(restart_len=m, max_iters=max_iters)
+    reps = []
+    for spec in ("1", "0"):
+        monkeypatch.setenv("KRY_SPECULATE", spec)
+        reps.append(kb.standard_gmres(op, b, None, cfg))
+    a, s = reps
+    assert (int(a.status), a.iterations, a.restarts, a.sync.reduces) == (int(s.status), s.iterations, s.restarts,
+                                                                        s.sync.reduces)
+    assert a.sync.per_block == s.sync.per_block and a.cycle_residuals == s.cycle_residuals
+    np.testing.assert_array_equal(a.solution, s.solution)
+
+
+def test_speculative_standard_gmres_lucky_breakdown(kb, ctx, monkeypatch):
+    """A column that vanishes exactly (A = 0: the first SpMV output is the
+    zero vector) fails its CholQR inside the queue; the solver redoes it on
+    the synchronous path and ends exactly as the synchronous run does."""
+    n = 64
+    rp = np.arange(n + 1, dtype=np.int64)
+    ci = np.arange(n, dtype=np.int64)
+    op = kb.CsrOperator(rp, ci, np.zeros(n))
+    b = np.linspace(1.0, 2.0, n)
+    cfg = kb.SolverConfig(restart_len=10, max_iters=40)
+    reps = []
+    for spec in ("1", "0"):
+        monkeypatch.setenv("KRY_SPECULATE", spec)
+        reps.append(kb.standard_gmres(op, b, None, cfg))
+    a, s = reps
+    assert (int(a.status), a.iterations, a.restarts, a.sync.reduces, a.breakdown) == (
+        int(s.status), s.iterations, s.restarts, s.sync.reduces, s.breakdown)
+    np.testing.assert_array_equal(a.solution, s.solution)

@@ -308,3 +308,47 @@ def test_graph_replay_matches_direct_launches(kb, ctx, ref, monkeypatch, key):
     assert a.cycle_residuals == b.cycle_residuals and a.sync.per_block == b.sync.per_block
     np.testing.assert_array_equal(a.solution, b.solution)
     assert a.telemetry["gpu_launches"] == b.telemetry["gpu_launches"]
+
+
+@pytest.mark.parametrize("case", ["lap2d_40_m30", "lap2d_64_m60", "lap3d_12_m40", "rand_3000_m50_jac"])
+def test_standard_gmres_matches_live_reference(kb, ctx, ref, case):
+    """standard_gmres (gmres.hpp:404-411: s = 1, BCGS2-CholQR2 = CGS2, 4
+    reduces per iteration) on the default — speculative — device path against
+    the live reference: identical status / iterations / restarts / reduces and
+    per-column sync deltas, every cycle's residual within the protocol (the
+    reference's FMA build gives the rounding envelope)."""
+    if case.startswith("lap2d"):
+        grid, m = (40, 30) if case == "lap2d_40_m30" else (64, 60)
+        a = ref.laplace2d(grid, grid)
+        op = kb.Laplace2D(grid, grid)
+        max_iters = 4 * m
+    elif case.startswith("lap3d"):
+        grid, m = 12, 40
+        a = ref.laplace3d(grid, grid, grid)
+        op = kb.Laplace3D(grid, grid, grid)
+        max_iters = 6 * m
+    else:
+        from oracle import randsparse
+        n, m = 3000, 50
+        rp, ci, vv = randsparse.random_sparse(n, 0, n, 30, seed=3, diag_factor=0.15, jacobi=True)  # D⁻¹A
+        a = ref.Csr(n, rp, ci, vv)
+        op = kb.CsrOperator(rp, ci, vv)
+        max_iters = 6 * m
+    b = ref.spmv(a, np.ones(a.n))
+    cfg_ref = ref.make_config(m=m, s=1, kind=1, max_iters=max_iters)
+    want = ref.solve(a, b, None, cfg_ref, standard=True)
+    got = kb.standard_gmres(op, b, None, kb.SolverConfig(restart_len=m, max_iters=max_iters))
+    assert (int(got.status), got.iterations, got.restarts, got.sync.reduces) == (
+        want.status, want.iterations, want.restarts, want.reduces)
+    assert got.sync.per_block == [int(v) for v in want.per_block]
+    saved = ref.lib()
+    ref._lib = ref._load(os.path.join(os.path.dirname(ref.__file__), "_ref", "libkrylov_ref_fma.so"))
+    try:
+        want_fma = ref.solve(a, b, None, cfg_ref, standard=True)
+    finally:
+        ref._lib = saved
+    c, f = np.array(want.cycle_residuals), np.array(want_fma.cycle_residuals)
+    env = np.abs(c - f) if len(c) == len(f) else np.full_like(c, np.inf)
+    tol = np.maximum(1e-10 * c, 10.0 * env) + ABS_FLOOR
+    assert len(got.cycle_residuals) == len(c)
+    assert (np.abs(np.array(got.cycle_residuals) - c) <= tol).all()

@@ -117,3 +117,21 @@ def test_bcgs2_breakdown_reports_pivot(kb, ctx, ref, rng):
     with pytest.raises(ref.RefError) as er:
         ref.bcgs2(q, v)
     assert e.value.pivot == er.value.pivot
+
+
+def test_bcgs2_abi_errors(kb, ctx, rng):
+    import ctypes as C
+    v = np.asfortranarray(rng.standard_normal((100, 3)))
+    q = np.zeros((100, 3), order="F")
+    rc = np.zeros((1, 3), order="F")
+    rj = np.zeros((3, 3), order="F")
+    piv, red = C.c_int64(0), C.c_int64(0)
+    P = kb._capi.P_dbl
+    p = lambda a: a.ctypes.data_as(P)
+    lib = kb.lib()
+    # unknown intra kind, negative prefix, zero width: status codes, never a crash
+    assert lib.kry_bcgs2(ctx.handle, 100, None, 0, p(v), 3, 7, p(q), p(rc), p(rj), C.byref(piv), C.byref(red)) != 0
+    assert lib.kry_bcgs2(ctx.handle, 100, None, -1, p(v), 3, 1, p(q), p(rc), p(rj), C.byref(piv), C.byref(red)) != 0
+    assert lib.kry_bcgs_project(ctx.handle, 100, None, 0, p(v), 0, p(q), p(rc), C.byref(red)) != 0
+    assert lib.kry_cholqr2(ctx.handle, 0, p(v), 3, p(q), p(rj), C.byref(piv), C.byref(red)) != 0
+    assert red.value == 0
